@@ -1,0 +1,164 @@
+/*
+ * lm_b200.h -- C ABI of the B200 (sm_100a) evaluation backend.
+ *
+ * This library replaces the reference's compute seam, the numba loop
+ * module lazymat/_loops.py (/root/reference/pkg/src/lazymat/_loops.py:15-407),
+ * one entry point per loop family.  The contract layer above it
+ * (checks, trace events, flop counts, rc -> exception mapping;
+ * lazymat/kernels.py) is mirrored in Python by
+ * paper_2502_03000_b200/kernels.py and calls these functions through
+ * ctypes (paper_2502_03000_b200/_native.py).
+ *
+ * Conventions:
+ *  - All pointers are DEVICE pointers owned by the caller; the library
+ *    never frees caller memory.  Internal scratch comes from the
+ *    stream-ordered allocator (cudaMallocAsync) on the caller's stream.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t, NULL = the
+ *    legacy default stream) and returns an int status:
+ *        0   queued successfully
+ *       <0   contract violation or CUDA error (lm_last_error() explains)
+ *    Singular-matrix results are reported asynchronously through a
+ *    device int32 `info` (0, or failing column + 1, exactly the
+ *    reference's rc convention, _loops.py:200-205).
+ *  - Matrices are strided views: element (i,j) is ptr[i*rs + j*cs]
+ *    (in elements) -- numpy's strides divided by the item size.  F-order
+ *    is rs=1, cs=rows; a transposed view swaps them; a diagonal vector
+ *    of an F-order square has stride rows+1.
+ *    Vectors are (ptr, n, stride).  No transpose flags: a view IS the
+ *    transposition (the reference planner never sets trans flags,
+ *    rewrite.py:628-629).
+ *  - dtype: LM_F64 (the reference's only element type, matrix.py:97)
+ *    or LM_F32 (extension, BASELINE configs 5).
+ *  - Arithmetic that the reference does element by element with one
+ *    rounding per operation (fused element-wise, diag scaling, LU
+ *    factor/solve, batched small LU, triangular and band solves) is
+ *    reproduced with the same operation order and NO FMA contraction, so
+ *    results are bit-identical.  Reductions over many terms (GEMM, GEMV,
+ *    SYRK, trace/diag of product) use parallel deterministic orders and
+ *    are within the north-star tolerance (normwise 1e-12 f64).
+ */
+#ifndef LM_B200_H
+#define LM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LM_ABI_VERSION 1
+
+enum { LM_F64 = 0, LM_F32 = 1 };
+
+typedef struct {
+    void *ptr;
+    int64_t rows, cols, rs, cs;
+} lm_view;
+
+typedef struct {
+    void *ptr;
+    int64_t n, stride;
+} lm_vec;
+
+/* ---- library ----------------------------------------------------------- */
+int lm_abi_version(void);
+/* Last error message of the calling thread ("" if none). */
+const char *lm_last_error(void);
+/* Number of kernels this library has launched since load (for the
+ * bench's gpu_launches claim). */
+int64_t lm_launch_count(void);
+
+/* ---- element-wise family: _loops.py:37-84 (_fused1.._fused4, _fused_axpy) */
+/* out = sum_k coeffs[k] * srcs[k], accumulated left to right per element,
+ * one rounding per multiply and per add (kernels.py:32-62). */
+int lm_fused_axpby(int dtype, int nterms, const double *coeffs, const lm_view *srcs, lm_view out,
+                   void *stream);
+
+/* Extension (Schur %, element /, abs, scalar +): postfix program over
+ * sources, one rounding per node -- the per-element semantics of
+ * naive_evaluate (expr.py:304-391) with R1 coefficient folding.
+ * ops: 0 LOAD src | 1 CONST idx | 2 ADD | 3 SUB | 4 MUL | 5 DIV | 6 ABS | 7 NEG.
+ * The program is JIT-compiled once per shape (NVRTC, sm_100a) into a
+ * single fused streaming kernel; constants are runtime arguments. */
+int lm_fused_program(int dtype, int nins, const int32_t *ops, const int32_t *args, int nconst,
+                     const double *consts, int nsrc, const lm_view *srcs, lm_view out, void *stream);
+
+/* The CUDA source generated for a program (inspection/tests).  Returns 0
+ * and fills buf, or the needed buffer size if buflen is too small. */
+int lm_program_source(int dtype, int flat, int nins, const int32_t *ops, const int32_t *args, int nconst,
+                      int nsrc, char *buf, int64_t buflen);
+
+/* dst = src (strided 2-D copy; the executor's RHS copy before solves,
+ * rewrite.py:653, and the naive arm's view extraction). */
+int lm_copy(int dtype, lm_view src, lm_view dst, void *stream);
+/* *d_result = sum of the strided vector v (deterministic tree). */
+int lm_vec_sum(int dtype, lm_vec v, void *d_result, void *stream);
+
+/* ---- products: _loops.py:87-121 (_gemm, _gemv, _gemv_t), :124-141 (_syrk) */
+/* out = a @ b (a p x q, b q x r).  r == 1 or p == 1 dispatch to the
+ * split-K GEMV kernel; otherwise the FP64 DMMA tensor-core GEMM. */
+int lm_gemm(int dtype, lm_view a, lm_view b, lm_view out, void *stream);
+/* out = a @ x (trans=0) or a.T @ x (trans=1) (kernels.py:88-103). */
+int lm_gemv(int dtype, lm_view a, lm_vec x, lm_vec out, int trans, void *stream);
+/* out = a @ a.T, upper triangle computed, lower mirrored bitwise. */
+int lm_syrk(int dtype, lm_view a, lm_view out, void *stream);
+
+/* ---- diagonal / reduction family: _loops.py:144-197 ------------------- */
+/* side 0: out[i,j] = d[i]*b[i,j];  side 1: out[i,j] = b[i,j]*d[j]. */
+int lm_diag_scale(int dtype, lm_vec d, lm_view b, int side, lm_view out, void *stream);
+/* out[i] = sum_k a[i,k]*b[k,i] (never forms a@b). */
+int lm_diag_of_product(int dtype, lm_view a, lm_view b, lm_vec out, void *stream);
+/* *d_result = sum_i sum_k a[i,k]*b[k,i]; d_result is one device element
+ * of `dtype` (written asynchronously, deterministic reduction tree). */
+int lm_trace_of_product(int dtype, lm_view a, lm_view b, void *d_result, void *stream);
+/* *d_result = sum_i a[i]*d[i]*c[i]. */
+int lm_triple_diag_dot(int dtype, lm_vec a, lm_vec d, lm_vec c, void *d_result, void *stream);
+
+/* ---- structure scan: _loops.py:15-34 (_analyze) ------------------------- */
+/* d_out[0] = lower bandwidth, d_out[1] = upper bandwidth, d_out[2] =
+ * symmetric (0/1; only meaningful when square).  Exact comparisons. */
+int lm_analyze(int dtype, lm_view a, int square, int64_t *d_out, void *stream);
+
+/* ---- factorisation and solves: _loops.py:200-388 ----------------------- */
+/* In-place LU with partial pivoting of the n x n F-order matrix `lu`
+ * (cs == rows, rs == 1).  d_piv[k] = pivot row of column k (0-based,
+ * sequential swap semantics), *d_info = 0 or failing column + 1. */
+int lm_lu_factor(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_info, void *stream);
+/* Solve with a factorisation from lm_lu_factor; x (n x m, F-order)
+ * arrives holding B and is overwritten with X. */
+int lm_lu_solve(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, void *stream);
+/* Banded solve (pack + factor + substitute) in place on x; kl/ku are
+ * the detected bandwidths.  ab_work: (2kl+ku+1) x n device scratch. */
+int lm_band_solve(int dtype, lm_view a, lm_view x, int64_t kl, int64_t ku, void *ab_work, int64_t *d_piv,
+                  int32_t *d_info, void *stream);
+/* Triangular solve in place (upper != 0: back substitution). */
+int lm_tri_solve(int dtype, lm_view a, lm_view x, int upper, int32_t *d_info, void *stream);
+
+/* ---- data movement: _loops.py:391-407 ------------------------------------ */
+int lm_transpose_copy(int dtype, lm_view a, lm_view out, void *stream);
+int lm_diag_materialise(int dtype, lm_vec d, lm_view out, void *stream);
+/* out = I (n x n), used by explicit_inverse (kernels.py:282-299). */
+int lm_set_identity(int dtype, lm_view out, void *stream);
+
+/* ---- batched entry points (new; no reference counterpart) -------------- */
+/* `batch` independent n x n systems A_b x_b = b_b, A stored F-order
+ * contiguous per instance (stride n*n), rhs one column per instance
+ * (stride n).  Exact reference op order (bit-identical to the per-
+ * instance lazymat lu_solve).  A is overwritten with its LU factors,
+ * x with the solution; d_piv: batch*n, d_info: batch. */
+int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, void *a, void *x, int64_t *d_piv,
+                        int32_t *d_info, void *stream);
+/* Batched structure classification of `batch` contiguous F-order n x n
+ * matrices: d_out[3*b + {0,1,2}] = lbw, ubw, sym. */
+int lm_analyze_batched(int dtype, int64_t n, int64_t batch, const void *a, int64_t *d_out, void *stream);
+/* Grouped size-class kernel for E_b = A_b.T @ B_b + C_b % D_b and
+ * s_b = trace(A_b @ B_b): all instances of one size n, contiguous per
+ * instance.  Reads each operand once. */
+int lm_expr_atb_schur_trace_batched(int dtype, int64_t n, int64_t batch, const void *a, const void *b,
+                                    const void *c, const void *d, void *e, void *s, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LM_B200_H */

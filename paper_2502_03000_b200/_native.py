@@ -1,0 +1,165 @@
+"""ctypes binding of the sm_100a C-ABI library (include/lm_b200.h).
+
+This is the drop-in seam: it takes the place of the reference's numba
+loop module (lazymat/_loops.py:15-407).  Operands are torch CUDA tensors
+of any stride -- torch is used only as the device-memory owner and for
+the current stream; all arithmetic happens in our kernels.  A call that
+fails in the library raises BackendError with the library's message.
+
+There is deliberately no CPU fallback: without a CUDA device (or
+without the built library) every compute entry point raises
+BackendUnavailableError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+import torch
+
+from .errors import BackendError, BackendUnavailableError
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "liblm_b200.so"
+
+F64, F32 = 0, 1
+
+# Every symbol include/lm_b200.h declares (checked by tests/test_boundary.py).
+EXPORTS = (
+    "lm_abi_version", "lm_last_error", "lm_launch_count",
+    "lm_fused_axpby", "lm_fused_program", "lm_program_source", "lm_copy", "lm_vec_sum",
+    "lm_gemm", "lm_gemv", "lm_syrk",
+    "lm_diag_scale", "lm_diag_of_product", "lm_trace_of_product", "lm_triple_diag_dot",
+    "lm_analyze", "lm_lu_factor", "lm_lu_solve", "lm_band_solve", "lm_tri_solve",
+    "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
+    "lm_lu_solve_batched", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched",
+)
+
+
+class View(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("rs", ctypes.c_int64), ("cs", ctypes.c_int64)]
+
+
+class Vec(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("n", ctypes.c_int64), ("stride", ctypes.c_int64)]
+
+
+_i, _i64, _p, _d = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_double
+_SIGS = {
+    "lm_abi_version": (_i, []),
+    "lm_last_error": (ctypes.c_char_p, []),
+    "lm_launch_count": (_i64, []),
+    "lm_fused_axpby": (_i, [_i, _i, ctypes.POINTER(_d), ctypes.POINTER(View), View, _p]),
+    "lm_fused_program": (_i, [_i, _i, _p, _p, _i, ctypes.POINTER(_d), _i, ctypes.POINTER(View), View, _p]),
+    "lm_program_source": (_i, [_i, _i, _i, _p, _p, _i, _i, ctypes.c_char_p, _i64]),
+    "lm_copy": (_i, [_i, View, View, _p]),
+    "lm_vec_sum": (_i, [_i, Vec, _p, _p]),
+    "lm_gemm": (_i, [_i, View, View, View, _p]),
+    "lm_gemv": (_i, [_i, View, Vec, Vec, _i, _p]),
+    "lm_syrk": (_i, [_i, View, View, _p]),
+    "lm_diag_scale": (_i, [_i, Vec, View, _i, View, _p]),
+    "lm_diag_of_product": (_i, [_i, View, View, Vec, _p]),
+    "lm_trace_of_product": (_i, [_i, View, View, _p, _p]),
+    "lm_triple_diag_dot": (_i, [_i, Vec, Vec, Vec, _p, _p]),
+    "lm_analyze": (_i, [_i, View, _i, _p, _p]),
+    "lm_lu_factor": (_i, [_i, View, _p, _p, _p]),
+    "lm_lu_solve": (_i, [_i, View, _p, View, _p]),
+    "lm_band_solve": (_i, [_i, View, View, _i64, _i64, _p, _p, _p, _p]),
+    "lm_tri_solve": (_i, [_i, View, View, _i, _p, _p]),
+    "lm_transpose_copy": (_i, [_i, View, View, _p]),
+    "lm_diag_materialise": (_i, [_i, Vec, View, _p]),
+    "lm_set_identity": (_i, [_i, View, _p]),
+    "lm_lu_solve_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p]),
+    "lm_analyze_batched": (_i, [_i, _i64, _i64, _p, _p, _p]),
+    "lm_expr_atb_schur_trace_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(require_device: bool = True):
+    """The ctypes handle; builds nothing.  ``require_device`` (default)
+    refuses to run without a CUDA device."""
+    global _lib
+    if require_device and not torch.cuda.is_available():
+        raise BackendUnavailableError(
+            "paper_2502_03000_b200 evaluates on a B200 (sm_100a) GPU only; no CUDA device is visible")
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not LIB_PATH.exists():
+                    raise BackendUnavailableError(
+                        f"C-ABI library not built ({LIB_PATH}); run `python -m paper_2502_03000_b200.build`")
+                lib = ctypes.CDLL(str(LIB_PATH))
+                for name, (res, args) in _SIGS.items():
+                    f = getattr(lib, name)
+                    f.restype = res
+                    f.argtypes = args
+                _lib = lib
+    return _lib
+
+
+def launch_count() -> int:
+    return int(load_library(False).lm_launch_count()) if LIB_PATH.exists() else 0
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.float64:
+        return F64
+    if t.dtype == torch.float32:
+        return F32
+    raise BackendError(f"unsupported element type {t.dtype}")
+
+
+def _dev_check(t: torch.Tensor):
+    if not t.is_cuda:
+        raise BackendUnavailableError(
+            "operand is not in device memory; this package has no CPU compute path")
+
+
+def view(t: torch.Tensor) -> View:
+    _dev_check(t)
+    if t.dim() != 2:
+        raise BackendError(f"2-D operand expected, got {t.dim()}-D")
+    r, c = t.shape
+    rs, cs = t.stride()
+    return View(t.data_ptr(), r, c, rs, cs)
+
+
+def vec(t: torch.Tensor) -> Vec:
+    _dev_check(t)
+    if t.dim() != 1:
+        raise BackendError(f"1-D operand expected, got {t.dim()}-D")
+    return Vec(t.data_ptr(), t.shape[0], t.stride(0))
+
+
+def stream_handle(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load_library(False).lm_last_error().decode(errors="replace")
+        raise BackendError(f"{what} failed (rc={rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    """Call a status-returning entry point on the current stream."""
+    lib = load_library()
+    rc = getattr(lib, name)(*args, ctypes.c_void_p(stream_handle()))
+    check(rc, name)
+
+
+def views(ts) -> ctypes.Array:
+    arr = (View * max(len(ts), 1))()
+    for k, t in enumerate(ts):
+        arr[k] = view(t)
+    return arr
+
+
+def doubles(xs) -> ctypes.Array:
+    xs = [float(x) for x in xs]
+    return (ctypes.c_double * max(len(xs), 1))(*xs)

@@ -1,0 +1,171 @@
+// common.cuh -- shared device/host helpers for the sm_100a backend.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "lm_b200.h"
+
+namespace lm {
+
+// ---- status / error plumbing ------------------------------------------------
+
+void set_error(const char *fmt, ...);
+void clear_error();
+void count_launch(int n = 1);
+int num_sms();
+
+#define LM_REQUIRE(cond, ...)                                                                 \
+    do {                                                                                      \
+        if (!(cond)) {                                                                        \
+            ::lm::set_error(__VA_ARGS__);                                                     \
+            return -1;                                                                        \
+        }                                                                                     \
+    } while (0)
+
+#define LM_CUDA(call)                                                                         \
+    do {                                                                                      \
+        cudaError_t _e = (call);                                                              \
+        if (_e != cudaSuccess) {                                                              \
+            ::lm::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+            return -2;                                                                        \
+        }                                                                                     \
+    } while (0)
+
+// After a <<<>>> launch.
+#define LM_LAUNCHED(n)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = cudaGetLastError();                                                  \
+        if (_e != cudaSuccess) {                                                              \
+            ::lm::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e));  \
+            return -2;                                                                        \
+        }                                                                                     \
+        ::lm::count_launch(n);                                                                \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Stream-ordered scratch (cudaMallocAsync); freed on the same stream.
+struct Scratch {
+    void *p = nullptr;
+    cudaStream_t s = nullptr;
+    Scratch() = default;
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    int alloc(size_t bytes, cudaStream_t st) {
+        s = st;
+        if (bytes == 0) bytes = 16;
+        cudaError_t e = cudaMallocAsync(&p, bytes, st);
+        if (e != cudaSuccess) {
+            set_error("cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
+            p = nullptr;
+            return -2;
+        }
+        return 0;
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    template <class T> T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+// ---- device-side strided views -----------------------------------------------
+
+template <class T> struct View {
+    T *p;
+    int64_t rows, cols, rs, cs;
+    __host__ __device__ T &operator()(int64_t i, int64_t j) const { return p[i * rs + j * cs]; }
+};
+
+template <class T> struct Vec {
+    T *p;
+    int64_t n, stride;
+    __host__ __device__ T &operator[](int64_t i) const { return p[i * stride]; }
+};
+
+template <class T> inline View<T> to_view(const lm_view &v) {
+    return View<T>{reinterpret_cast<T *>(v.ptr), v.rows, v.cols, v.rs, v.cs};
+}
+template <class T> inline Vec<T> to_vec(const lm_vec &v) {
+    return Vec<T>{reinterpret_cast<T *>(v.ptr), v.n, v.stride};
+}
+
+inline bool f_contig(const lm_view &v) { return v.rs == 1 && (v.cs == v.rows || v.cols == 1); }
+
+// ---- exactly rounded scalar ops (no FMA contraction, whatever the flags) ----
+
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float rsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float rdiv(float a, float b) { return __fdiv_rn(a, b); }
+
+// ---- streaming loads / stores ---------------------------------------------------
+
+__device__ __forceinline__ double2 ld_stream(const double2 *p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ float4 ld_stream(const float4 *p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) {
+    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_stream(float4 *p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+                 "f"(v.w)
+                 : "memory");
+}
+
+template <class T> struct Vec16;  // 16-byte vector of T
+template <> struct Vec16<double> {
+    using type = double2;
+    static constexpr int N = 2;
+};
+template <> struct Vec16<float> {
+    using type = float4;
+    static constexpr int N = 4;
+};
+
+// ---- warp / block reductions ------------------------------------------------------
+
+template <class T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = radd(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Deterministic block sum (fixed tree): every thread returns the total.
+template <class T, int NT> __device__ T block_sum(T v, T *smem /* >= NT/32 */) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) smem[wid] = v;
+    __syncthreads();
+    T t = (threadIdx.x < NT / 32) ? smem[threadIdx.x] : T(0);
+    if (wid == 0) {
+#pragma unroll
+        for (int o = NT / 64; o > 0; o >>= 1) t = radd(t, __shfl_xor_sync(0xffffffffu, t, o));
+        if (lane == 0) smem[0] = t;
+    }
+    __syncthreads();
+    return smem[0];
+}
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// shared launch helpers (elementwise.cu)
+bool is_linear(const lm_view &v);  // enumerates its elements in F-order, unit step
+int ew_grid(int64_t work_items);   // grid for 256-thread streaming kernels
+
+}  // namespace lm

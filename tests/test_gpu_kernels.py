@@ -1,0 +1,313 @@
+"""Kernel-level parity: every C-ABI kernel against the C oracle
+(oracle/lm_oracle.c, itself pinned bitwise to the reference) on seeded
+inputs, including strided / transposed views and edge shapes (1x1,
+n x 1, 1 x n, non-multiples of every tile size, empty)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_03000_b200 as lm
+from oracle import lm_oracle as O
+from paper_2502_03000_b200 import kernels as K
+from paper_2502_03000_b200.matrix import fortran_empty
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def dev(a: np.ndarray) -> torch.Tensor:
+    """numpy array / view -> device tensor with identical strides."""
+    a = np.asarray(a)
+    if a.ndim == 1:
+        return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    if a.flags.f_contiguous:
+        return torch.from_numpy(np.ascontiguousarray(a.T)).to(DEV).t()
+    assert a.flags.c_contiguous
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+_strided = dev
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+def bits_equal(x, y):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return x.shape == y.shape and np.array_equal(x.view(np.int64), y.view(np.int64))
+
+
+def normwise(x, y):
+    scale = max(float(np.max(np.abs(y))) if y.size else 0.0, 1e-300)
+    return float(np.max(np.abs(x - y))) / scale if y.size else 0.0
+
+
+SHAPES = [(1, 1), (1, 7), (7, 1), (5, 3), (33, 17), (64, 64), (100, 37), (129, 255)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("nterms", [1, 2, 3, 5, 9])
+def test_fused_axpby_bitwise(shape, nterms):
+    rng = np.random.default_rng(hash((shape, nterms)) % 2**32)
+    srcs = [np.asfortranarray(rng.uniform(-1, 1, shape)) for _ in range(nterms)]
+    if nterms >= 3 and shape[0] > 1 and shape[1] > 1:
+        srcs[1] = np.ascontiguousarray(rng.uniform(-1, 1, shape[::-1])).T  # transposed view
+    coeffs = list(rng.uniform(-3, 3, nterms))
+    ref = np.zeros(shape, order="F")
+    O.fused(coeffs, srcs, ref)
+    out = fortran_empty(*shape, device=DEV)
+    K.fused_axpby_n(coeffs, [dev(s) for s in srcs], out)
+    assert bits_equal(host(out), ref)
+
+
+PROGS = [
+    ("x0 c0 * x1 x2 * + x0 x1 abs c1 + / -", 3, [2.0, 1.0]),  # BASELINE config 1
+    ("x0 x1 *", 2, []),
+    ("x0 x1 /", 2, []),
+    ("x0 abs", 1, []),
+    ("c0 x0 /", 1, [3.0]),
+    ("x0 c0 + x1 neg *", 2, [-0.5]),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("prog", PROGS, ids=lambda p: p[0])
+def test_fused_program_bitwise(shape, prog):
+    text, nsrc, consts = prog
+    rng = np.random.default_rng(11)
+    srcs = [np.asfortranarray(rng.uniform(-1, 1, shape)) for _ in range(nsrc)]
+    ops, args, *_ = K.parse_program(text)
+    ref = np.zeros(shape, order="F")
+    O.program(ops.numpy(), args.numpy(), consts, srcs, ref)
+    out = fortran_empty(*shape, device=DEV)
+    K.fused_expr(text, consts, [dev(s) for s in srcs], out)
+    assert bits_equal(host(out), ref)
+
+
+def test_fused_program_strided_path_bitwise():
+    rng = np.random.default_rng(12)
+    a = np.ascontiguousarray(rng.uniform(-1, 1, (40, 30))).T  # 30x40 transposed view
+    b = np.asfortranarray(rng.uniform(-1, 1, (30, 40)))
+    ops, args, *_ = K.parse_program("x0 x1 * x1 abs +")
+    ref = np.zeros((30, 40), order="F")
+    O.program(ops.numpy(), args.numpy(), [], [a, b], ref)
+    out = fortran_empty(30, 40, device=DEV)
+    K.fused_expr("x0 x1 * x1 abs +", [], [dev(a), dev(b)], out)
+    assert bits_equal(host(out), ref)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("side", ["left", "right"])
+def test_diag_scale_bitwise(shape, side):
+    rng = np.random.default_rng(3)
+    b = np.asfortranarray(rng.uniform(-1, 1, shape))
+    n = shape[0] if side == "left" else shape[1]
+    sq = np.asfortranarray(rng.uniform(-1, 1, (n, n)))
+    d = np.diagonal(sq)  # strided diagonal view (stride n+1)
+    ref = np.zeros(shape, order="F")
+    O.diag_scale(np.ascontiguousarray(d), b, side, ref)
+    out = fortran_empty(*shape, device=DEV)
+    K.diag_scale(torch.diagonal(dev(sq)), dev(b), side, out)
+    assert bits_equal(host(out), ref)
+
+
+@pytest.mark.parametrize("pq", [(1, 1), (1, 9), (9, 1), (31, 33), (64, 64), (100, 250), (257, 129)])
+@pytest.mark.parametrize("bt", [False, True])
+def test_trace_and_diag_of_product(pq, bt):
+    p, q = pq
+    rng = np.random.default_rng(p * 1000 + q)
+    a = np.asfortranarray(rng.uniform(-1, 1, (p, q)))
+    b = np.asfortranarray(rng.uniform(-1, 1, (q, p))) if not bt else np.ascontiguousarray(rng.uniform(-1, 1, (p, q))).T
+    tref = O.trace_of_product(a, b)
+    dref = np.zeros(p)
+    O.diag_of_product(a, b, dref)
+    t = K.trace_of_product(dev(a), dev(b))
+    assert abs(t - tref) <= 1e-12 * max(abs(tref), np.sum(np.abs(dref)) * 1e-3, 1e-300)
+    d = torch.empty(p, dtype=torch.float64, device=DEV)
+    K.diag_of_product(dev(a), dev(b), d)
+    assert normwise(host(d), dref) <= 1e-12
+
+
+def test_trace_is_run_to_run_bitwise_reproducible():
+    rng = np.random.default_rng(5)
+    a = dev(np.asfortranarray(rng.uniform(-1, 1, (777, 555))))
+    b = dev(np.asfortranarray(rng.uniform(-1, 1, (555, 777))))
+    vals = {K.trace_of_product(a, b) for _ in range(5)}
+    assert len(vals) == 1
+
+
+def test_triple_diag_dot():
+    rng = np.random.default_rng(6)
+    a, d, c = (rng.uniform(-1, 1, 1001) for _ in range(3))
+    ref = O.triple_diag_dot(a, d, c)
+    got = K.triple_diag_dot(*(torch.from_numpy(x).to(DEV) for x in (a, d, c)))
+    assert abs(got - ref) <= 1e-12 * max(abs(ref), 1.0)
+
+
+GEMM_SHAPES = [(1, 1, 1), (7, 5, 1), (1, 5, 7), (4096, 64, 1), (13, 17, 19), (64, 64, 64), (100, 8000, 100),
+               (8000, 100, 100), (130, 70, 90)]
+
+
+@pytest.mark.parametrize("pqr", GEMM_SHAPES)
+@pytest.mark.parametrize("layout", ["NN", "TN", "NT"])
+def test_gemm_normwise(pqr, layout):
+    p, q, r = pqr
+    rng = np.random.default_rng(p + 7 * q + 13 * r)
+    a = np.asfortranarray(rng.uniform(-1, 1, (p, q))) if layout[0] == "N" else \
+        np.asfortranarray(rng.uniform(-1, 1, (q, p))).T
+    b = np.asfortranarray(rng.uniform(-1, 1, (q, r))) if layout[1] == "N" else \
+        np.asfortranarray(rng.uniform(-1, 1, (r, q))).T
+    ref = np.zeros((p, r), order="F")
+    O.gemm(a, b, ref)
+    out = fortran_empty(p, r, device=DEV)
+    K.gemm(dev(a), dev(b), out)
+    assert normwise(host(out), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("nk", [(1, 1), (5, 3), (31, 7), (64, 64), (130, 300), (200, 1000)])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_syrk_normwise_and_bitwise_symmetric(nk, transposed):
+    n, k = nk
+    rng = np.random.default_rng(n * 31 + k)
+    a = np.asfortranarray(rng.uniform(-1, 1, (n, k))) if not transposed else \
+        np.asfortranarray(rng.uniform(-1, 1, (k, n))).T
+    ref = np.zeros((n, n), order="F")
+    O.syrk(a, ref)
+    out = fortran_empty(n, n, device=DEV)
+    K.syrk(dev(a), out)
+    h = host(out)
+    assert normwise(h, ref) <= 1e-12
+    assert bits_equal(h, h.T)
+
+
+@pytest.mark.parametrize("pq", [(1, 1), (7, 5), (4096, 4096), (300, 2000)])
+@pytest.mark.parametrize("trans", [False, True])
+def test_gemv_normwise(pq, trans):
+    p, q = pq
+    rng = np.random.default_rng(p + q)
+    a = np.asfortranarray(rng.uniform(-1, 1, (p, q)))
+    x = rng.uniform(-1, 1, p if trans else q)
+    ref = np.zeros(q if trans else p)
+    O.gemv(a, x, ref, trans)
+    out = torch.empty(ref.shape[0], dtype=torch.float64, device=DEV)
+    K.gemv(_strided(a), torch.from_numpy(x).to(DEV), out, trans)
+    assert normwise(host(out), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 17, 64, 65, 100, 200, 333])
+@pytest.mark.parametrize("kind", ["general", "dominant"])
+def test_lu_factor_bitwise_values_and_pivots(n, kind):
+    """The blocked GPU LU reproduces the reference's unblocked getf2
+    exactly: same pivots (real pivoting on general matrices), same bits."""
+    rng = np.random.default_rng(n)
+    a = np.asfortranarray(rng.uniform(-1, 1, (n, n)) + (n * np.eye(n) if kind == "dominant" else 0))
+    rc, lu_ref, piv_ref = O.lu_factor(a)
+    assert rc == 0
+    lu, piv = K.lu_factor(_strided(a))
+    assert np.array_equal(host(piv), piv_ref)
+    assert bits_equal(host(lu.data), lu_ref)
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, 3)))
+    x_ref = np.array(b, order="F")
+    O.lu_solve(lu_ref, piv_ref, x_ref)
+    x = _strided(np.array(b, order="F"))
+    K.lu_solve_into(_strided(a), x)
+    assert bits_equal(host(x), x_ref)
+
+
+def test_lu_singular_column_reported_with_balanced_workspace():
+    a = np.zeros((3, 3), order="F")
+    a[0, 0] = 1.0
+    a[2, 2] = 1.0
+
+    def attempt():
+        try:
+            K.lu_factor(_strided(a))
+        except lm.SingularMatrixError as e:
+            return e
+        return None
+
+    tr = lm.with_trace(attempt)
+    assert tr.result is not None and tr.result.column == 1
+    assert len([e for e in tr.events if e.kind == "alloc"]) == len([e for e in tr.events if e.kind == "free"]) == 1
+
+
+@pytest.mark.parametrize("n", [4, 9, 27, 100])
+def test_band_solve_bitwise(n):
+    rng = np.random.default_rng(n)
+    for kl, ku in [(0, 0), (1, 1), (2, 1), (3, 3)]:
+        a = rng.uniform(-1, 1, (n, n))
+        i, j = np.indices((n, n))
+        a[(i - j > kl) | (j - i > ku)] = 0.0
+        a[np.diag_indices(n)] += n
+        a = np.asfortranarray(a)
+        b = np.asfortranarray(rng.uniform(-1, 1, (n, 2)))
+        xr = np.array(b, order="F")
+        assert O.band_solve(a, xr, kl, ku) == 0
+        x = _strided(np.array(b, order="F"))
+        K.band_solve_into(_strided(a), x, kl, ku)
+        assert bits_equal(host(x), xr)
+
+
+@pytest.mark.parametrize("upper", [True, False])
+def test_triangular_solve_bitwise(upper):
+    rng = np.random.default_rng(4)
+    n = 70
+    a = rng.uniform(-1, 1, (n, n))
+    a = np.triu(a) if upper else np.tril(a)
+    a[np.diag_indices(n)] += n
+    a = np.asfortranarray(a)
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, 3)))
+    b[5, 0] = 0.0
+    xr = np.array(b, order="F")
+    assert O.tri_solve(a, xr, upper) == 0
+    x = _strided(np.array(b, order="F"))
+    K.triangular_solve_into(_strided(a), x, upper)
+    assert bits_equal(host(x), xr)
+    a[3, 3] = 0.0
+    with pytest.raises(lm.SingularMatrixError) as e:
+        K.triangular_solve_into(_strided(np.asfortranarray(a)), _strided(np.array(b, order="F")), upper)
+    assert e.value.column == 3
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 6), (6, 1), (13, 13), (40, 33), (64, 64), (97, 97)])
+def test_analyze_exact(shape):
+    rng = np.random.default_rng(sum(shape))
+    for trial in range(6):
+        a = rng.normal(size=shape)
+        a[rng.random(size=shape) < 0.6] = 0.0
+        if trial % 2 and shape[0] == shape[1]:
+            a = a + a.T
+        a = np.asfortranarray(a)
+        square = shape[0] == shape[1]
+        lbw, ubw, sym = O.analyze(a, square)
+        info = lm.analyze_structure(_strided(a))
+        assert (info.lower_bandwidth, info.upper_bandwidth) == (lbw, ubw)
+        assert info.is_symmetric == (square and sym)
+
+
+def test_transpose_copy_and_diag_materialise_exact():
+    rng = np.random.default_rng(8)
+    a = np.asfortranarray(rng.uniform(-1, 1, (37, 61)))
+    out = fortran_empty(61, 37, device=DEV)
+    K.transpose_copy(_strided(a), out)
+    assert bits_equal(host(out), a.T)
+    d = rng.uniform(-1, 1, 45)
+    m = fortran_empty(45, 45, device=DEV)
+    K.diag_materialise(torch.from_numpy(d).to(DEV), m)
+    assert bits_equal(host(m), np.diag(d))
+
+
+def test_explicit_inverse_matches_solve_against_identity():
+    rng = np.random.default_rng(14)
+    n = 17
+    a = np.asfortranarray(rng.uniform(0, 1, (n, n)) + n * np.eye(n))
+    rc, lu, piv = O.lu_factor(a)
+    ref = np.asfortranarray(np.eye(n))
+    O.lu_solve(lu, piv, ref)
+    out = fortran_empty(n, n, device=DEV)
+    K.explicit_inverse_into(_strided(a), out)
+    assert bits_equal(host(out), ref)
