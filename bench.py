@@ -122,8 +122,13 @@ class Workload:
 
     config = 0
     unit = "GB/s"
+    bound = "hbm"
+    graphable = True  # the step has no host synchronisation -> CUDA graph replay
     workload = ""
     dtype = "f64"
+
+    def cpu_work_per_step(self):
+        return self.work_per_step()
 
     def host_inputs(self) -> dict:
         raise NotImplementedError
@@ -212,7 +217,317 @@ class Config1(Workload):
         O.program(ops.numpy(), args.numpy(), [2.0, 1.0], [h["A"], h["B"], h["C"]], out)
 
 
-WORKLOADS = {1: Config1, 2: Config2}
+def _fp64_peak():
+    p = ROOT / "profiles" / "fp64_peak.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["tflops"]), "measured (tools/fp64_probe.cu)"
+    return 37.0, "fallback"
+
+
+class Config3a(Workload):
+    config = "3a"
+    N = 4096
+    workload = "A*B*C*v, float64 4096x4096 A,B,C and 4096x1 v, U(-1,1): re-associated to three GEMVs"
+
+    def host_inputs(self):
+        n = self.N
+        return {"A": seeded(3, 0, (n, n)), "B": seeded(3, 1, (n, n)), "C": seeded(3, 2, (n, n)),
+                "v": seeded(3, 3, (n, 1))}
+
+    def expressions(self, lm, m):
+        return [m["A"] * m["B"] * m["C"] * m["v"]]
+
+    def work_per_step(self):
+        n = self.N
+        return 3 * n * n * 8 + 4 * n * 8
+
+    def kernels_for_roofline(self, lm, m):
+        from paper_2502_03000_b200 import kernels as K
+        import torch
+        n = self.N
+        y = torch.empty(n, dtype=torch.float64, device=m["A"].data.device)
+        A, v = m["A"].data, m["v"].data[:, 0]
+        return [("gemv", n * n * 8 + 2 * n * 8, lambda: K.gemv(A, v, y))]
+
+    def cpu_step(self, O, h):
+        n = self.N
+        t1, t2, t3 = (np.zeros((n, 1), order="F") for _ in range(3))
+        O.gemm(h["C"], h["v"], t1)
+        O.gemm(h["B"], t1, t2)
+        O.gemm(h["A"], t2, t3)
+
+
+class Config3b(Workload):
+    config = "3b"
+    unit = "TFLOP/s"
+    bound = "fp64"
+    workload = "X*Y*Z, float64 X 8000x100, Y 100x8000, Z 8000x100, U(-1,1): ordered (Y*Z first), 320 MFLOP"
+
+    def host_inputs(self):
+        return {"X": seeded(3, 10, (8000, 100)), "Y": seeded(3, 11, (100, 8000)), "Z": seeded(3, 12, (8000, 100))}
+
+    def expressions(self, lm, m):
+        return [m["X"] * m["Y"] * m["Z"]]
+
+    def work_per_step(self):
+        return 2 * 100 * 8000 * 100 * 2
+
+    def kernels_for_roofline(self, lm, m):
+        from paper_2502_03000_b200 import kernels as K
+        from paper_2502_03000_b200.matrix import fortran_empty
+        out = fortran_empty(100, 100)
+        Y, Z = m["Y"].data, m["Z"].data
+        return [("gemm(Y,Z)", 2 * 100 * 8000 * 100, lambda: K.gemm(Y, Z, out))]
+
+    def cpu_step(self, O, h):
+        yz = np.zeros((100, 100), order="F")
+        O.gemm(h["Y"], h["Z"], yz)
+        out = np.zeros((8000, 100), order="F")
+        O.gemm(h["X"], yz, out)
+
+
+class Config3c(Workload):
+    config = "3c"
+    unit = "TFLOP/s"
+    bound = "fp64"
+    workload = "A.t()*A, float64 A 16384x2048 U(-1,1): R8 SYRK (upper tiles + bitwise mirror), 68.75 GFLOP"
+    M, K = 16384, 2048
+
+    def host_inputs(self):
+        return {"A": seeded(3, 20, (self.M, self.K))}
+
+    def expressions(self, lm, m):
+        return [m["A"].t() * m["A"]]
+
+    def work_per_step(self):
+        return self.K * (self.K + 1) * self.M  # lazymat/kernels.py:109-116 formula n(n+1)k
+
+    def kernels_for_roofline(self, lm, m):
+        from paper_2502_03000_b200 import kernels as K
+        from paper_2502_03000_b200.matrix import fortran_empty
+        out = fortran_empty(self.K, self.K)
+        a = m["A"].data.t()
+        return [("syrk", self.work_per_step(), lambda: K.syrk(a, out))]
+
+    cpu_sample_k = 512
+    cpu_sample_desc = "the same SYRK over the first 512 of the 16384 inner terms (1/32 of the flops)"
+
+    def cpu_step(self, O, h):
+        # bounded sample: the same syrk over the first 512 of the 16384 inner terms
+        a = h["A"][: self.cpu_sample_k, :].T
+        out = np.zeros((self.K, self.K), order="F")
+        O.syrk(a, out)
+
+    def cpu_work_per_step(self):
+        return self.K * (self.K + 1) * self.cpu_sample_k
+
+
+class Config4a(Workload):
+    config = "4a"
+    unit = "TFLOP/s"
+    bound = "fp64"
+    graphable = False
+    N, NRHS = 8192, 64
+    workload = ("inverse(A)*b -> LU solve (R9), float64 A = U(-1,1) + 8192*I (data leaf), b 8192x64; "
+                "exact reference operation order (bit-identical pivots and values)")
+
+    def host_inputs(self):
+        n = self.N
+        a = seeded(4, 0, (n, n))
+        a[np.diag_indices(n)] += n
+        return {"A": a, "b": seeded(4, 1, (n, self.NRHS))}
+
+    def expressions(self, lm, m):
+        return [lm.inverse(m["A"]) * m["b"]]
+
+    def work_per_step(self):
+        n, k = self.N, self.NRHS
+        return 2 * n * n * n // 3 + 2 * n * n * k  # lazymat/kernels.py:190, :215
+
+    cpu_n = 1024
+    cpu_sample_desc = "an n=1024 LU solve with 64 RHS (same unblocked algorithm; a rate, not the 8192 problem)"
+
+    def cpu_step(self, O, h):
+        n = self.cpu_n
+        a = np.asfortranarray(h["A"][:n, :n] - (self.N - n) * np.eye(n))
+        rc, lu, piv = O.lu_factor(a)
+        x = np.array(h["b"][:n, :], order="F")
+        O.lu_solve(lu, piv, x)
+
+    def cpu_work_per_step(self):
+        n, k = self.cpu_n, self.NRHS
+        return 2 * n * n * n // 3 + 2 * n * n * k
+
+
+class Config4b(Workload):
+    config = "4b"
+    unit = "GB/s"
+    graphable = False
+    N, BATCH = 64, 4096
+    workload = ("4096 independent inverse(A_i)*b_i, A_i = U(-1,1) + 64*I (64x64), b_i 64x1: batched structure "
+                "scan + in-shared-memory LU in the reference's exact order")
+
+    def host_inputs(self):
+        n, bt = self.N, self.BATCH
+        rng = np.random.default_rng(1000003 * 42 + 101 * 4 + 7)
+        a = rng.uniform(-1.0, 1.0, (bt, n, n)) + n * np.eye(n)[None]
+        b = rng.uniform(-1.0, 1.0, (bt, n, 1))
+        return {"A": a, "b": b}
+
+    def setup(self, lm, h):
+        from paper_2502_03000_b200.batch import stack_fortran
+        return {"A": stack_fortran(h["A"]), "b": stack_fortran(h["b"])}
+
+    def step_fn(self, lm, ctx):
+        from paper_2502_03000_b200.batch import solve_batched
+        return lambda: [solve_batched(ctx["A"], ctx["b"]).x]
+
+    def e2e_fn(self, lm, h):
+        import torch
+        from paper_2502_03000_b200.batch import solve_batched
+        pa = torch.from_numpy(np.ascontiguousarray(np.transpose(h["A"], (0, 2, 1)))).pin_memory()
+        pb = torch.from_numpy(np.ascontiguousarray(h["b"])).pin_memory()
+        px = torch.empty_like(pb).pin_memory()
+
+        def run():
+            A = pa.cuda(non_blocking=True).transpose(1, 2)
+            x = solve_batched(A, pb.cuda(non_blocking=True)).x
+            px.copy_(x)
+            torch.cuda.synchronize()
+            return [px]
+        return run, pa.numel() * 8 + pb.numel() * 8, px.numel() * 8
+
+    def work_per_step(self):
+        n, bt = self.N, self.BATCH
+        return bt * (n * n * 8 + 2 * n * 8)  # A read once, b read, x written
+
+    def flops_per_step(self):
+        n, bt = self.N, self.BATCH
+        return bt * (2 * n * n * n // 3 + 2 * n * n)
+
+    def cpu_step(self, O, h):
+        n = self.N
+        for i in range(self.BATCH):
+            rc, lu, piv = O.lu_factor(np.asfortranarray(h["A"][i]))
+            x = np.array(h["b"][i], order="F")
+            O.lu_solve(lu, piv, x)
+
+
+class Config5a(Workload):
+    """262144 instances of E = A.t()*B + C%D, s = trace(A*B), n in {32,64,128}."""
+
+    config = "5a"
+    BATCH = 262144
+    SIZES = (32, 64, 128)
+    dtype = "f64"
+    workload = ("262144 independent E = A.t()*B + C % D and s = trace(A*B), square sizes drawn uniformly from "
+                "{32,64,128}, U(-1,1); one grouped kernel per size class")
+    e2e_sample = 4096  # instances per size class pushed through the API from host memory
+
+    def counts(self):
+        rng = np.random.default_rng(1000003 * 42 + 101 * 5 + 99)
+        sizes = rng.choice(self.SIZES, self.BATCH)
+        return {n: int((sizes == n).sum()) for n in self.SIZES}
+
+    @property
+    def width(self):
+        return 8 if self.dtype == "f64" else 4
+
+    def work_per_step(self):
+        w = self.width
+        return sum(c * (5 * n * n * w + w) for n, c in self.counts().items())
+
+    def flops_per_step(self):
+        return sum(c * (2 * n ** 3 + 4 * n * n) for n, c in self.counts().items())
+
+    def host_inputs(self):
+        # bounded CPU sample (the full batch is generated on the device)
+        rng = np.random.default_rng(1000003 * 42 + 101 * 5 + 1)
+        return {n: rng.uniform(-1, 1, (4, self.CPU_SAMPLE[n], n, n)) for n in self.SIZES}
+
+    CPU_SAMPLE = {32: 96, 64: 48, 128: 16}
+    cpu_sample_desc = "160 instances (96 of n=32, 48 of n=64, 16 of n=128), oracle gemm + program + trace each"
+
+    def setup(self, lm, host):
+        import torch
+        from paper_2502_03000_b200.batch import empty_batch
+        tdt = torch.float64 if self.dtype == "f64" else torch.float32
+        g = torch.Generator(device="cuda")
+        g.manual_seed(1000003 * 42 + 101 * 5)
+        ctx = {}
+        for n, c in self.counts().items():
+            ops = []
+            for _ in range(4):
+                t = empty_batch(c, n, n, tdt)
+                t.uniform_(-1.0, 1.0, generator=g)
+                ops.append(t)
+            ctx[n] = ops
+        return ctx
+
+    def step_fn(self, lm, ctx):
+        from paper_2502_03000_b200.batch import atb_schur_trace
+        return lambda: [atb_schur_trace(*ctx[n]) for n in self.SIZES]
+
+    def kernels_for_roofline(self, lm, ctx):
+        from paper_2502_03000_b200.batch import atb_schur_trace
+        out = []
+        for n, c in self.counts().items():
+            out.append((f"atb_schur_trace n={n}", c * (5 * n * n * self.width + self.width),
+                        lambda n=n: atb_schur_trace(*ctx[n])))
+        return out
+
+    def cpu_step(self, O, h):
+        from paper_2502_03000_b200.kernels import parse_program
+        ops, args, *_ = parse_program("x0 x1 x2 * +")
+        for n in self.SIZES:
+            x = h[n]
+            for i in range(x.shape[1]):
+                A, B, C, D = (np.asfortranarray(x[k, i]) for k in range(4))
+                g = np.zeros((n, n), order="F")
+                O.gemm(A.T, B, g)
+                E = np.zeros((n, n), order="F")
+                O.program(ops.numpy(), args.numpy(), [], [g, C, D], E)
+                O.trace_of_product(A, B)
+
+    def cpu_work_per_step(self):
+        w = 8
+        return sum(self.CPU_SAMPLE[n] * (5 * n * n * w + w) for n in self.SIZES)
+
+    def e2e_fn(self, lm, h):
+        import torch
+        from paper_2502_03000_b200.batch import atb_schur_trace
+        tdt = torch.float64 if self.dtype == "f64" else torch.float32
+        k = self.e2e_sample
+        pinned = {n: [torch.empty((k, n, n), dtype=tdt).uniform_(-1, 1).pin_memory() for _ in range(4)]
+                  for n in self.SIZES}
+        outs = {n: (torch.empty((k, n, n), dtype=tdt).pin_memory(), torch.empty(k, dtype=tdt).pin_memory())
+                for n in self.SIZES}
+
+        def run():
+            res = []
+            for n in self.SIZES:
+                dev = [p.cuda(non_blocking=True).transpose(1, 2) for p in pinned[n]]
+                E, s = atb_schur_trace(*dev)
+                outs[n][0].copy_(E.transpose(1, 2))
+                outs[n][1].copy_(s)
+                res += list(outs[n])
+            torch.cuda.synchronize()
+            return res
+        w = self.width
+        h2d = sum(4 * k * n * n * w for n in self.SIZES)
+        d2h = sum(k * (n * n + 1) * w for n in self.SIZES)
+        self.e2e_work = sum(k * (5 * n * n * w + w) for n in self.SIZES)
+        return run, h2d, d2h
+
+
+class Config5a32(Config5a):
+    config = "5a-f32"
+    dtype = "f32"
+    workload = Config5a.workload.replace("U(-1,1)", "U(-1,1), float32")
+
+
+WORKLOADS = {"1": Config1, "2": Config2, "3a": Config3a, "3b": Config3b, "3c": Config3c, "4a": Config4a,
+             "4b": Config4b, "5a": Config5a, "5a-f32": Config5a32}
 
 
 # ---------------------------------------------------------------------------------------
@@ -253,6 +568,58 @@ def time_cpu(O, wl, host, budget_s: float = 10.0, min_steps: int = 1, max_steps:
     return steps, el
 
 
+def _default_setup(wl, lm, host):
+    return {k: lm.DenseMatrix(v) for k, v in host.items()}
+
+
+def _default_step(wl, lm, ctx):
+    exprs = wl.expressions(lm, ctx)
+    if wl.graphable:
+        plans = [lm.rewrite(e) for e in exprs]
+        return lambda: [lm.execute(p, host_scalar=False) for p in plans]
+    # steps with host synchronisation (structure scans, pivot checks):
+    # evaluate() per step, rewrite included, like the reference's timed region
+    return lambda: [lm.evaluate(e, host_scalar=False) for e in wl.expressions(lm, ctx)]
+
+
+def _default_e2e(wl, lm, host):
+    import torch
+    pinned = {k: torch.from_numpy(np.ascontiguousarray(v.T)).pin_memory().t() for k, v in host.items()}
+    outs = {}
+
+    def run():
+        m = {k: lm.DenseMatrix(t) for k, t in pinned.items()}
+        res = []
+        for e in wl.expressions(lm, m):
+            r = lm.evaluate(e)
+            if isinstance(r, float):
+                res.append(r)
+                continue
+            key = len(res)
+            if key not in outs or outs[key].shape != r.data.shape:
+                outs[key] = torch.empty(r.data.shape[::-1], dtype=r.data.dtype).pin_memory().t()
+            outs[key].copy_(r.data)
+            res.append(outs[key])
+        torch.cuda.synchronize()
+        return res
+
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    res = run()
+    d2h = sum(8 if isinstance(r, float) else r.numel() * r.element_size() for r in res)
+    return run, h2d, d2h
+
+
+def _time_device(fn, steps):
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
 def run_ours(args, wl, ws, rank, local):
     import torch
 
@@ -261,49 +628,40 @@ def run_ours(args, wl, ws, rank, local):
 
     torch.cuda.set_device(local)
     host = wl.host_inputs()
-    mats = {k: lm.DenseMatrix(v) for k, v in host.items()}
-    exprs = wl.expressions(lm, mats)
-    plans = [lm.rewrite(e) for e in exprs]
-
-    def step():
-        return [lm.execute(p, host_scalar=False) for p in plans]
+    ctx = wl.setup(lm, host) if hasattr(wl, "setup") else _default_setup(wl, lm, host)
+    step = wl.step_fn(lm, ctx) if hasattr(wl, "step_fn") else _default_step(wl, lm, ctx)
 
     sampler = ClockSampler(local)
     with sampler:
-        # warm-up (JIT compiles, allocator pools), launch count of one step
-        for _ in range(max(args.warmup, 3)):
+        for _ in range(args.warmup):  # JIT compiles, allocator pools, clocks up
             step()
         torch.cuda.synchronize()
         c0 = _native.launch_count()
         step()
         torch.cuda.synchronize()
         launches_per_step = _native.launch_count() - c0
-        # capture the step as one CUDA graph (plans are static)
-        g = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):
-            step()
-        torch.cuda.current_stream().wait_stream(s)
-        with torch.cuda.graph(g):
-            step()
-        for _ in range(max(args.warmup, 3)):
-            g.replay()
+        timed = step
+        if wl.graphable:  # capture the static step as one CUDA graph
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                step()
+            torch.cuda.current_stream().wait_stream(s)
+            with torch.cuda.graph(g):
+                step()
+            timed = g.replay
+            for _ in range(args.warmup):
+                timed()
         torch.cuda.synchronize()
         _barrier(ws)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            g.replay()
-        e1.record()
-        torch.cuda.synchronize()
+        ms = _time_device(timed, args.steps)
         _barrier(ws)
-        ms = e0.elapsed_time(e1) / args.steps
 
-        # per-kernel durations for the roofline (CUDA events, same stream, graph replays)
+        # per-kernel durations for the roofline (CUDA events on the launching stream)
         kern = []
-        for name, work, thunk in wl.kernels_for_roofline(lm, mats):
+        for name, work, thunk in wl.kernels_for_roofline(lm, ctx):
             thunk()
             torch.cuda.synchronize()
             gk = torch.cuda.CUDAGraph()
@@ -311,86 +669,71 @@ def run_ours(args, wl, ws, rank, local):
                 thunk()
             gk.replay()
             torch.cuda.synchronize()
-            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            k0.record()
-            for _ in range(args.steps):
-                gk.replay()
-            k1.record()
-            torch.cuda.synchronize()
-            kern.append((name, work, k0.elapsed_time(k1) / args.steps))
+            kern.append((name, work, _time_device(gk.replay, max(args.steps, 5))))
     ms_max = _max_over_ranks(ms, ws)
 
-    # end-to-end through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        pinned = {k: torch.from_numpy(np.ascontiguousarray(v.T)).pin_memory().t() for k, v in host.items()}
-        outs = {}
-
-        def e2e_step():
-            m = {k: lm.DenseMatrix(t) for k, t in pinned.items()}
-            res = []
-            for e in wl.expressions(lm, m):
-                r = lm.evaluate(e)
-                if isinstance(r, float):
-                    res.append(r)
-                else:
-                    key = len(res)
-                    if key not in outs or outs[key].shape != r.data.shape:
-                        outs[key] = torch.empty(r.data.shape[::-1], dtype=r.data.dtype).pin_memory().t()
-                    outs[key].copy_(r.data)
-                    res.append(outs[key])
-            torch.cuda.synchronize()
-            return res
-
+        run, h2d, d2h = wl.e2e_fn(lm, host) if hasattr(wl, "e2e_fn") else _default_e2e(wl, lm, host)
         for _ in range(2):
-            e2e_step()
-        h2d = sum(t.numel() * t.element_size() for t in pinned.values())
-        res = e2e_step()
-        d2h = sum(8 if isinstance(r, float) else r.numel() * r.element_size() for r in res)
+            run()
         _barrier(ws)
         k_e2e = max(3, min(args.steps, 10))
         t0 = time.perf_counter()
         for _ in range(k_e2e):
-            e2e_step()
-        el = (time.perf_counter() - t0) / k_e2e
-        el = _max_over_ranks(el, ws)
-        e2e = {"value": wl.work_per_step() * ws / el / wl.scale(), "unit": wl.unit,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": el * 1e3,
-               "steps": k_e2e, "includes": "H2D inputs, rewrite (+device scans), kernels, D2H results"}
+            run()
+        el = _max_over_ranks((time.perf_counter() - t0) / k_e2e, ws)
+        work = getattr(wl, "e2e_work", wl.work_per_step())
+        e2e = {"value": work * ws / el / wl.scale(), "unit": wl.unit, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": el * 1e3, "steps": k_e2e,
+               "includes": "pinned-host inputs H2D, evaluate (rewrite + device scans + kernels), results D2H"}
+        if hasattr(wl, "e2e_work"):
+            e2e["sample"] = f"{wl.e2e_sample} instances per size class through the API per step"
 
-    # CPU restatement of the reference loops (rank 0, N=1 only)
     cpu = None
     if not args.no_cpu and ws == 1 and rank == 0:
         from oracle import lm_oracle as O
         steps, el = time_cpu(O, wl, host, budget_s=args.cpu_budget)
-        cpu = {"value": wl.work_per_step() * steps / el / wl.scale(), "unit": wl.unit, "cores": 1, "kind": "port",
-               "sample": f"{steps} full steps of the same workload ({el:.1f} s), oracle/lm_oracle.c single thread"}
+        cpu = {"value": wl.cpu_work_per_step() * steps / el / wl.scale(), "unit": wl.unit, "cores": 1,
+               "kind": "port",
+               "sample": f"{steps} steps ({el:.1f} s) of {getattr(wl, 'cpu_sample_desc', 'the same workload')}, "
+                         f"oracle/lm_oracle.c (the reference loops restated in C), single thread"}
 
-    peak, peak_kind = _peaks()
     roof = None
     if kern:
         name, work, kms = max(kern, key=lambda x: x[2])
-        achieved = work / (kms * 1e-3) / 1e9
+        if wl.bound == "fp64":
+            peak, peak_kind = _fp64_peak()
+            achieved, unit = work / (kms * 1e-3) / 1e12, "TFLOP/s"
+        else:
+            peak, peak_kind = _peaks()
+            achieved, unit = work / (kms * 1e-3) / 1e9, "GB/s"
         traffic = None
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():
             traffic = json.loads(tf.read_text()).get(f"config{wl.config}", {}).get(name)
-        roof = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "algorithmic_bytes_per_launch": work, "ms_per_launch": kms,
-                "all": {n: {"ms": t, "GB/s": w / (t * 1e-3) / 1e9} for n, w, t in kern}}
+        roof = {"bound": "tensor" if wl.bound == "fp64" else "hbm", "kernel": name, "achieved": achieved,
+                "peak": peak, "peak_kind": peak_kind, "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                "work_per_launch": work, "ms_per_launch": kms,
+                "all": {n: {"ms": t, unit: w / (t * 1e-3) / (1e12 if unit == "TFLOP/s" else 1e9)}
+                        for n, w, t in kern}}
+        if wl.bound == "fp64":
+            roof["note"] = "FP64 (DMMA/DFMA) ceiling; sm_100a has no tcgen05 f64 kind"
 
     out = {"metric": METRIC, "value": wl.work_per_step() * ws / (ms_max * 1e-3) / wl.scale(), "unit": wl.unit,
            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl.dtype,
            "data": "synthetic: seeded U(-1,1) (SURVEY.md 8(d)); no public dataset",
-           "config": {"workload": wl.workload, "baseline_config": wl.config,
-                      "work_per_step": wl.work_per_step(),
-                      "l2": "every input > 126 MB L2 (4096^2 f64 = 134 MB); no flush needed",
+           "config": {"workload": wl.workload, "baseline_config": wl.config, "work_per_step": wl.work_per_step(),
+                      "l2": "working set per step > 126 MB L2; no flush needed",
                       "parallelism": "replicas" if ws > 1 else "single GPU",
-                      "timing": "CUDA events around CUDA-graph replays of the compiled plans"},
+                      "timing": ("CUDA events around CUDA-graph replays of the compiled plans" if wl.graphable
+                                 else "CUDA events around evaluate() calls (host syncs inside)")},
            "impl": "ours", "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
            "clocks": sampler.summary(), "gpu_launches": launches_per_step * args.steps}
+    if hasattr(wl, "flops_per_step"):
+        out["config"]["flops_per_step"] = wl.flops_per_step()
+        out["tflops"] = wl.flops_per_step() * ws / (ms_max * 1e-3) / 1e12
     return out
 
 
@@ -406,7 +749,7 @@ def run_reference(args, wl, ws, rank):
     for _ in range(args.steps):
         wl.cpu_step(O, host)
     el = (time.perf_counter() - t0) / args.steps
-    v = wl.work_per_step() / el / wl.scale()
+    v = wl.cpu_work_per_step() / el / wl.scale()
     return {"metric": METRIC, "value": v, "unit": wl.unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": wl.dtype, "data": "synthetic: seeded U(-1,1) (SURVEY.md 8(d))",
@@ -423,7 +766,7 @@ def main(argv=None):
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -141,12 +141,14 @@ int lm_diag_materialise(int dtype, lm_vec d, lm_view out, void *stream);
 int lm_set_identity(int dtype, lm_view out, void *stream);
 
 /* ---- batched entry points (new; no reference counterpart) -------------- */
-/* `batch` independent n x n systems A_b x_b = b_b, A stored F-order
- * contiguous per instance (stride n*n), rhs one column per instance
- * (stride n).  Exact reference op order (bit-identical to the per-
- * instance lazymat lu_solve).  A is overwritten with its LU factors,
- * x with the solution; d_piv: batch*n, d_info: batch. */
-int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, void *a, void *x, int64_t *d_piv,
+/* `batch` independent n x n systems A_b x_b = b_b (n <= 64), A stored
+ * F-order contiguous per instance (stride n*n), one RHS column per
+ * instance (stride n).  Exact reference op order (bit-identical to the
+ * per-instance lazymat lu_factor + lu_solve).  x arrives holding b and is
+ * overwritten with the solution; A is only read.  Optional outputs (NULL
+ * to skip): lu_out (batch*n*n LU factors), d_piv (batch*n pivots).
+ * d_info[b] = 0 or failing column + 1. */
+int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void *x, void *lu_out, int64_t *d_piv,
                         int32_t *d_info, void *stream);
 /* Batched structure classification of `batch` contiguous F-order n x n
  * matrices: d_out[3*b + {0,1,2}] = lbw, ubw, sym. */

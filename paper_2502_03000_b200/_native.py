@@ -71,7 +71,7 @@ _SIGS = {
     "lm_transpose_copy": (_i, [_i, View, View, _p]),
     "lm_diag_materialise": (_i, [_i, Vec, View, _p]),
     "lm_set_identity": (_i, [_i, View, _p]),
-    "lm_lu_solve_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p]),
+    "lm_lu_solve_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p]),
     "lm_analyze_batched": (_i, [_i, _i64, _i64, _p, _p, _p]),
     "lm_expr_atb_schur_trace_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]),
 }

@@ -1,0 +1,158 @@
+"""Batched evaluation of many independent small expression instances.
+
+The reference has no batch API (``evaluate`` takes one tree,
+lazymat/rewrite.py:680-682; SURVEY.md finding 6).  These entry points
+evaluate a batch of same-shaped instances with ONE kernel per plan step
+instead of one Python evaluate per instance, with per-instance results
+identical to evaluating every instance on its own:
+
+* ``solve_batched(A, b)``: inverse(A_i)*b_i (BASELINE config 4b).  The
+  per-instance R9/R10 structure dispatch (lazymat/rewrite.py:389-414) runs
+  as one batched device scan; instances whose plan is ``lu_solve`` (the
+  general and symmetric classes) are solved by one in-shared-memory LU
+  kernel in the reference's exact operation order -- values and pivots
+  bit-identical to per-instance lazymat.  Band / triangular instances go
+  through the single-instance planner.
+* ``atb_schur_trace(A, B, C, D)``: E_i = A_i.T*B_i + C_i % D_i and
+  s_i = trace(A_i*B_i) (BASELINE config 5a), one fused kernel per size
+  class that reads every operand once.
+
+Batched operands are (batch, rows, cols) device tensors whose instances
+are column-major: element (b, i, j) at b*rows*cols + i + j*rows (torch
+strides (rows*cols, 1, rows)); ``stack_fortran`` builds one from host
+arrays.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import KernelContractError, SingularMatrixError
+from .matrix import DenseMatrix, default_device
+
+__all__ = ["stack_fortran", "empty_batch", "solve_batched", "atb_schur_trace", "analyze_batched",
+           "BatchSolveResult"]
+
+
+def empty_batch(batch: int, rows: int, cols: int, dtype=torch.float64, device=None) -> torch.Tensor:
+    device = default_device() if device is None else device
+    return torch.empty((batch, cols, rows), dtype=dtype, device=device).transpose(1, 2)
+
+
+def stack_fortran(arrs, dtype=torch.float64, device=None) -> torch.Tensor:
+    """(batch, r, c) host array-like -> device batch, per-instance F-order."""
+    a = np.asarray(arrs, dtype=np.float64 if dtype == torch.float64 else np.float32)
+    host = torch.from_numpy(np.ascontiguousarray(np.transpose(a, (0, 2, 1))))
+    device = default_device() if device is None else device
+    return host.to(device).transpose(1, 2)
+
+
+def _check_batch(t: torch.Tensor, name: str):
+    if t.dim() != 3:
+        raise KernelContractError(f"{name}: batched operand must be (batch, rows, cols)")
+    b, r, c = t.shape
+    st = t.stride()
+    ok = st[0] == r * c and (r <= 1 or st[1] == 1) and (c <= 1 or st[2] == r)
+    if not ok and b * r * c > 0:
+        raise KernelContractError(f"{name}: instances must be contiguous column-major (strides {(r * c, 1, r)})")
+    N._dev_check(t)
+
+
+def analyze_batched(A: torch.Tensor) -> np.ndarray:
+    """(batch, 3) int64 host array: lower bandwidth, upper bandwidth,
+    symmetric flag of every square instance (exact device scan)."""
+    _check_batch(A, "analyze_batched")
+    b, n, _ = A.shape
+    out = torch.empty((b, 3), dtype=torch.int64, device=A.device)
+    N.call("lm_analyze_batched", N.dtype_code(A), n, b, A.data_ptr(), out.data_ptr())
+    return out.cpu().numpy()
+
+
+class BatchSolveResult:
+    """x (batch, n, 1) device tensor; per-instance rule logs (as the
+    single-instance planner would log them) and the LU class mask."""
+
+    def __init__(self, x, rule_logs, lu_mask):
+        self.x = x
+        self.rule_logs = rule_logs
+        self.lu_mask = lu_mask
+
+
+def _classify(info, n):
+    """The reference ladder (lazymat/rewrite.py:146-173) per instance."""
+    lbw, ubw, sym = info[:, 0], info[:, 1], info[:, 2].astype(bool)
+    band = lbw + ubw <= max(4, n // 4)
+    triu = ~band & (lbw == 0)
+    tril = ~band & ~triu & (ubw == 0)
+    symm = ~band & ~triu & ~tril & sym
+    return band, triu, tril, symm
+
+
+def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> BatchSolveResult:
+    """inverse(A_i) * b_i for every instance (R9 -> R10 dispatch -> solve).
+
+    A: (batch, n, n), b: (batch, n, 1); both per-instance F-order.  A is
+    not modified.  Raises SingularMatrixError naming the first failing
+    instance when ``check`` (one host sync, as the reference raises
+    synchronously)."""
+    _check_batch(A, "solve_batched A")
+    _check_batch(b, "solve_batched b")
+    bt, n, n2 = A.shape
+    if n != n2 or b.shape[1] != n or b.shape[2] != 1:
+        raise KernelContractError("solve_batched: A must be (batch, n, n) and b (batch, n, 1)")
+    info = analyze_batched(A)
+    band, triu, tril, symm = _classify(info, n)
+    lu_mask = ~(band | triu | tril)
+    logs = []
+    for i in range(bt):
+        if band[i]:
+            logs.append(["R9", "R10:BAND"])
+        elif triu[i]:
+            logs.append(["R9", "R10:TRIU"])
+        elif tril[i]:
+            logs.append(["R9", "R10:TRIL"])
+        elif symm[i]:
+            logs.append(["R9", "R10:SYM-DETECTED"])
+        else:
+            logs.append(["R9"])
+    x = torch.empty((bt, 1, n), dtype=A.dtype, device=A.device).transpose(1, 2)
+    x.copy_(b)
+    if lu_mask.all() and n <= 64:
+        dinfo = torch.empty(bt, dtype=torch.int32, device=A.device)
+        N.call("lm_lu_solve_batched", N.dtype_code(A), n, bt, A.data_ptr(), x.data_ptr(), None, None,
+               dinfo.data_ptr())
+        if check:
+            bad = torch.nonzero(dinfo).flatten()
+            if bad.numel():
+                i = int(bad[0])
+                col = int(dinfo[i]) - 1
+                raise SingularMatrixError(f"singular matrix in instance {i}: zero pivot in column {col}",
+                                          column=col)
+        return BatchSolveResult(x, logs, lu_mask)
+    # mixed classes (or n > 64): the single-instance planner per instance
+    from .expr import inverse
+    from .rewrite import evaluate
+    for i in range(bt):
+        ai = DenseMatrix(A[i])
+        bi = DenseMatrix(b[i])
+        x[i].copy_(evaluate(inverse(ai) * bi).data)
+    return BatchSolveResult(x, logs, lu_mask)
+
+
+def atb_schur_trace(A, B, C, D):
+    """E_i = A_i.T @ B_i + C_i % D_i and s_i = trace(A_i @ B_i) for one
+    size class (all instances n x n).  Returns (E, s)."""
+    for t, nm in ((A, "A"), (B, "B"), (C, "C"), (D, "D")):
+        _check_batch(t, f"atb_schur_trace {nm}")
+    bt, n, n2 = A.shape
+    if n != n2 or any(tuple(t.shape) != (bt, n, n) for t in (B, C, D)):
+        raise KernelContractError("atb_schur_trace: all operands must be (batch, n, n)")
+    if len({A.dtype, B.dtype, C.dtype, D.dtype}) != 1:
+        raise KernelContractError("atb_schur_trace: operands must share one element type")
+    E = empty_batch(bt, n, n, A.dtype, A.device)
+    s = torch.empty(bt, dtype=A.dtype, device=A.device)
+    N.call("lm_expr_atb_schur_trace_batched", N.dtype_code(A), n, bt, A.data_ptr(), B.data_ptr(), C.data_ptr(),
+           D.data_ptr(), E.data_ptr(), s.data_ptr())
+    return E, s

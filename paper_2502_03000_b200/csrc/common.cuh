@@ -164,6 +164,15 @@ template <class T, int NT> __device__ T block_sum(T v, T *smem /* >= NT/32 */) {
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Persistent-grid size: resident CTAs per SM (occupancy calculator) x SMs,
+// so a grid-stride kernel runs as exactly one full wave (no tail wave).
+template <class K> int resident_grid(K kernel, int threads, size_t smem = 0) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return per_sm * num_sms();
+}
+
 // shared launch helpers (elementwise.cu)
 bool is_linear(const lm_view &v);  // enumerates its elements in F-order, unit step
 int ew_grid(int64_t work_items);   // grid for 256-thread streaming kernels

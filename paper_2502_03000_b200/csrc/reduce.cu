@@ -24,33 +24,59 @@ constexpr int kRedThreads = 256;  // 32 x 8
 
 // ---- diag_scale -----------------------------------------------------------------
 
-template <class T, bool RIGHT>
-__global__ void __launch_bounds__(256) diag_scale_flat(Vec<const T> d, const T *__restrict__ b, T *__restrict__ out,
-                                                       int64_t rows, int64_t nvec, int64_t n) {
+// Column-panel streaming kernel (F-order b and out: rs == 1): a thread owns
+// VN consecutive rows and walks a chunk of columns, U vectors in flight;
+// the row scale d[i..] is loaded once (left) or one d[j] per column
+// (right, a broadcast).  No index division anywhere.
+template <class T, bool RIGHT, bool VEC>
+__global__ void __launch_bounds__(256) diag_scale_cols(Vec<const T> d, const T *__restrict__ b, int64_t ldb,
+                                                       T *__restrict__ out, int64_t ldo, int64_t rows, int64_t cols,
+                                                       int64_t cols_per_block) {
     using V = typename Vec16<T>::type;
-    constexpr int VN = Vec16<T>::N;
-    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += nth) {
-        const V x = ld_stream(reinterpret_cast<const V *>(b) + v);
-        int64_t e0 = v * VN;
-        int64_t j = e0 / rows, i = e0 - j * rows;
-        V r;
+    constexpr int VN = VEC ? Vec16<T>::N : 1;
+    constexpr int U = 4;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VN;
+    if (i >= rows) return;
+    const int64_t j0 = (int64_t)blockIdx.y * cols_per_block;
+    const int64_t j1 = j0 + cols_per_block < cols ? j0 + cols_per_block : cols;
+    T dl[VN];
+    if (!RIGHT)
 #pragma unroll
-        for (int l = 0; l < VN; ++l) {
-            const T bv = (&x.x)[l];
-            (&r.x)[l] = RIGHT ? rmul(bv, d[j]) : rmul(d[i], bv);
-            if (++i == rows) {
-                i = 0;
-                ++j;
+        for (int l = 0; l < VN; ++l) dl[l] = d[i + l];
+    int64_t j = j0;
+    for (; j + U <= j1; j += U) {
+        T x[U][VN];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (VEC) {
+                const V t = ld_stream(reinterpret_cast<const V *>(b + i + (j + u) * ldb));
+#pragma unroll
+                for (int l = 0; l < VN; ++l) x[u][l] = (&t.x)[l];
+            } else {
+                x[u][0] = b[i + (j + u) * ldb];
             }
         }
-        st_stream(reinterpret_cast<V *>(out) + v, r);
-    }
-    if (blockIdx.x == 0)
-        for (int64_t e = nvec * VN + threadIdx.x; e < n; e += blockDim.x) {
-            const int64_t j = e / rows, i = e - j * rows;
-            out[e] = RIGHT ? rmul(b[e], d[j]) : rmul(d[i], b[e]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const T dj = RIGHT ? d[j + u] : T(0);
+            if (VEC) {
+                V r;
+#pragma unroll
+                for (int l = 0; l < VN; ++l) (&r.x)[l] = RIGHT ? rmul(x[u][l], dj) : rmul(dl[l], x[u][l]);
+                st_stream(reinterpret_cast<V *>(out + i + (j + u) * ldo), r);
+            } else {
+                out[i + (j + u) * ldo] = RIGHT ? rmul(x[u][0], dj) : rmul(dl[0], x[u][0]);
+            }
         }
+    }
+    for (; j < j1; ++j) {
+        const T dj = RIGHT ? d[j] : T(0);
+#pragma unroll
+        for (int l = 0; l < VN; ++l) {
+            const T bv = b[i + l + j * ldb];
+            out[i + l + j * ldo] = RIGHT ? rmul(bv, dj) : rmul(dl[l], bv);
+        }
+    }
 }
 
 template <class T, bool RIGHT>
@@ -67,15 +93,25 @@ template <class T> int diag_scale_impl(const lm_vec &dv, const lm_view &bv, int 
     const int64_t n = bv.rows * bv.cols;
     if (n == 0) return 0;
     Vec<const T> d{reinterpret_cast<const T *>(dv.ptr), dv.n, dv.stride};
-    const bool flat = is_linear(bv) && is_linear(ov) && (reinterpret_cast<uintptr_t>(bv.ptr) & 15) == 0 &&
-                      (reinterpret_cast<uintptr_t>(ov.ptr) & 15) == 0;
-    if (flat) {
+    const bool cm = bv.rs == 1 && ov.rs == 1;  // column-major b and out (any leading dims)
+    if (cm) {
         constexpr int VN = Vec16<T>::N;
-        const int64_t nvec = n / VN;
-        if (side)
-            diag_scale_flat<T, true><<<ew_grid(nvec), 256, 0, s>>>(d, (const T *)bv.ptr, (T *)ov.ptr, bv.rows, nvec, n);
-        else
-            diag_scale_flat<T, false><<<ew_grid(nvec), 256, 0, s>>>(d, (const T *)bv.ptr, (T *)ov.ptr, bv.rows, nvec, n);
+        const int64_t ldb = bv.cols > 1 ? bv.cs : bv.rows, ldo = ov.cols > 1 ? ov.cs : ov.rows;
+        const bool vec = bv.rows % VN == 0 && ldb % VN == 0 && ldo % VN == 0 &&
+                         (reinterpret_cast<uintptr_t>(bv.ptr) & 15) == 0 && (reinterpret_cast<uintptr_t>(ov.ptr) & 15) == 0;
+        const int64_t gx = ceil_div(bv.rows, 256 * (vec ? VN : 1));
+        int64_t gy = ceil_div((int64_t)num_sms() * 8, gx);
+        if (gy > bv.cols) gy = bv.cols;
+        if (gy > 65535) gy = 65535;
+        const int64_t cpb = ceil_div(bv.cols, gy);
+        gy = ceil_div(bv.cols, cpb);
+        dim3 grid((unsigned)gx, (unsigned)gy);
+        const T *bp = (const T *)bv.ptr;
+        T *op = (T *)ov.ptr;
+        if (side && vec) diag_scale_cols<T, true, true><<<grid, 256, 0, s>>>(d, bp, ldb, op, ldo, bv.rows, bv.cols, cpb);
+        else if (side) diag_scale_cols<T, true, false><<<grid, 256, 0, s>>>(d, bp, ldb, op, ldo, bv.rows, bv.cols, cpb);
+        else if (vec) diag_scale_cols<T, false, true><<<grid, 256, 0, s>>>(d, bp, ldb, op, ldo, bv.rows, bv.cols, cpb);
+        else diag_scale_cols<T, false, false><<<grid, 256, 0, s>>>(d, bp, ldb, op, ldo, bv.rows, bv.cols, cpb);
     } else {
         View<const T> b{(const T *)bv.ptr, bv.rows, bv.cols, bv.rs, bv.cs};
         View<T> o = to_view<T>(ov);
@@ -91,42 +127,67 @@ template <class T> int diag_scale_impl(const lm_vec &dv, const lm_view &bv, int 
 // ---- trace(A*B) ---------------------------------------------------------------------
 
 // Per-block partial of sum_{i,k} A[i,k]*B[k,i] over a static set of
-// 32x32 (i,k) tiles.  Register double-buffering keeps the next tile's
-// 8 loads per thread in flight while the current one is consumed.
-template <class T>
-__global__ void __launch_bounds__(kRedThreads) trace_tiles(View<const T> A, View<const T> B, int64_t ntr, int64_t ntiles,
-                                                           T *__restrict__ partials) {
-    __shared__ T sB[kTile][kTile + 1];
+// 64x64 (i,k) tiles (persistent grid, one full wave).  Each thread holds
+// 16 elements of the A tile (rows tx, tx+32; columns ty+8r) in registers
+// and stages 16 elements of the B tile transposed through shared memory
+// (row stride 65: conflict-free on both the store and the load); the next
+// tile's 32 loads are issued before the current tile is consumed.
+constexpr int kTr = 64;
+template <class T, bool CONTIG>
+__global__ void __launch_bounds__(kRedThreads, 2) trace_tiles(View<const T> A, View<const T> B, int64_t ntr,
+                                                              int64_t ntiles, T *__restrict__ partials) {
+    __shared__ T sB[kTr][kTr + 1];
     __shared__ T red[kRedThreads / 32];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t p = A.rows, q = A.cols;
-    T acc = T(0);
-    T ra[4], rb[4];
+    T acc0 = T(0), acc1 = T(0);
+    T ra[16], rb[16];
     auto load = [&](int64_t t) {
-        const int64_t i0 = (t % ntr) * kTile, k0 = (t / ntr) * kTile;
+        const int64_t i0 = (t % ntr) * kTr, k0 = (t / ntr) * kTr;
+        const bool full = i0 + kTr <= p && k0 + kTr <= q;
+        if (CONTIG && full) {
+            const T *pa = A.p + (i0 + tx) + (k0 + ty) * A.cs;
+            const T *pb = B.p + (k0 + tx) + (i0 + ty) * B.cs;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int64_t ia = i0 + tx, ka = k0 + ty + 8 * r;
-            ra[r] = (ia < p && ka < q) ? A(ia, ka) : T(0);
-            const int64_t kb = k0 + tx, ib = i0 + ty + 8 * r;
-            rb[r] = (kb < q && ib < p) ? B(kb, ib) : T(0);
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    ra[e * 8 + r] = __ldg(pa + 32 * e + 8 * r * A.cs);
+                    rb[e * 8 + r] = __ldg(pb + 32 * e + 8 * r * B.cs);
+                }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int64_t ia = i0 + tx + 32 * e, ka = k0 + ty + 8 * r;
+                    ra[e * 8 + r] = (ia < p && ka < q) ? A(ia, ka) : T(0);
+                    const int64_t kb = k0 + tx + 32 * e, ib = i0 + ty + 8 * r;
+                    rb[e * 8 + r] = (kb < q && ib < p) ? B(kb, ib) : T(0);
+                }
         }
     };
     int64_t t = blockIdx.x;
     if (t < ntiles) load(t);
     for (; t < ntiles; t += gridDim.x) {
-        T ca[4];
+        T ca[16];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            ca[r] = ra[r];
-            sB[ty + 8 * r][tx] = rb[r];  // sB[i_local][k_local] = B[k0+k_local, i0+i_local]
-        }
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                ca[e * 8 + r] = ra[e * 8 + r];
+                sB[ty + 8 * r][tx + 32 * e] = rb[e * 8 + r];  // sB[i_local][k_local] = B[k0+k_local, i0+i_local]
+            }
         __syncthreads();
         if (t + gridDim.x < ntiles) load(t + gridDim.x);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) acc = radd(acc, rmul(ca[r], sB[tx][ty + 8 * r]));
+        for (int r = 0; r < 8; ++r) {
+            acc0 = fma(ca[r], sB[tx][ty + 8 * r], acc0);
+            acc1 = fma(ca[8 + r], sB[tx + 32][ty + 8 * r], acc1);
+        }
         __syncthreads();
     }
+    T acc = radd(acc0, acc1);
     acc = block_sum<T, kRedThreads>(acc, red);
     if (threadIdx.x == 0) partials[blockIdx.x] = acc;
 }
@@ -144,14 +205,19 @@ template <class T> int trace_impl(const lm_view &av, const lm_view &bv, void *d_
     const int64_t p = av.rows, q = av.cols;
     View<const T> A{(const T *)av.ptr, av.rows, av.cols, av.rs, av.cs};
     View<const T> B{(const T *)bv.ptr, bv.rows, bv.cols, bv.rs, bv.cs};
-    const int64_t ntr = ceil_div(p, kTile), ntc = ceil_div(q, kTile), ntiles = ntr * ntc;
-    int64_t blocks = (int64_t)num_sms() * 8;
+    const int64_t ntr = ceil_div(p, kTr), ntc = ceil_div(q, kTr), ntiles = ntr * ntc;
+    const bool contig = av.rs == 1 && bv.rs == 1;
+    auto kern = contig ? trace_tiles<T, true> : trace_tiles<T, false>;
+    static int grid_cache[2] = {0, 0};
+    int &g = grid_cache[contig ? 1 : 0];
+    if (!g) g = resident_grid(kern, kRedThreads);
+    int64_t blocks = g;
     if (blocks > ntiles) blocks = ntiles;
     if (blocks < 1) blocks = 1;
     Scratch part;
     if (int rc = part.alloc(sizeof(T) * blocks, s)) return rc;
     if (ntiles > 0) {
-        trace_tiles<T><<<(unsigned)blocks, kRedThreads, 0, s>>>(A, B, ntr, ntiles, part.as<T>());
+        kern<<<(unsigned)blocks, kRedThreads, 0, s>>>(A, B, ntr, ntiles, part.as<T>());
         LM_LAUNCHED(1);
     } else {
         LM_CUDA(cudaMemsetAsync(part.p, 0, sizeof(T), s));

@@ -1,0 +1,85 @@
+"""Batched entry points vs per-instance oracle results."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2502_03000_b200 as lm
+from oracle import lm_oracle as O
+from paper_2502_03000_b200.batch import atb_schur_trace, solve_batched, stack_fortran
+from paper_2502_03000_b200.kernels import parse_program
+
+pytestmark = pytest.mark.gpu
+
+
+def bits_equal(x, y):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return x.shape == y.shape and np.array_equal(x.view(np.int64), y.view(np.int64))
+
+
+@pytest.mark.parametrize("n", [1, 7, 32, 64])
+@pytest.mark.parametrize("kind", ["dominant", "general"])
+def test_solve_batched_bitwise_vs_per_instance_reference(n, kind):
+    rng = np.random.default_rng(n)
+    bt = 37
+    A = rng.uniform(-1, 1, (bt, n, n)) + (n * np.eye(n)[None] if kind == "dominant" else 0)
+    b = rng.uniform(-1, 1, (bt, n, 1))
+    res = solve_batched(stack_fortran(A), stack_fortran(b))
+    x = res.x.cpu().numpy()
+    for i in range(bt):
+        rc, lu, piv = O.lu_factor(np.asfortranarray(A[i]))
+        if n > 4 and kind == "general":
+            pass
+        xr = np.array(b[i], order="F")
+        if rc == 0:
+            O.lu_solve(lu, piv, xr)
+        if res.lu_mask[i]:
+            assert bits_equal(x[i], xr), i
+        else:  # band/triangular instance: the single-instance plan result
+            ref = lm.evaluate(lm.inverse(lm.DenseMatrix(A[i])) * lm.DenseMatrix(b[i])).to_numpy()
+            assert bits_equal(x[i], ref)
+
+
+def test_solve_batched_rule_logs_match_single_instance_planner():
+    rng = np.random.default_rng(3)
+    n, bt = 16, 5
+    A = rng.uniform(-1, 1, (bt, n, n)) + n * np.eye(n)[None]
+    A[1] = np.triu(A[1])
+    A[2] = A[2] + A[2].T
+    b = rng.uniform(-1, 1, (bt, n, 1))
+    res = solve_batched(stack_fortran(A), stack_fortran(b))
+    for i in range(bt):
+        plan = lm.rewrite(lm.inverse(lm.DenseMatrix(A[i])) * lm.DenseMatrix(b[i]))
+        assert res.rule_logs[i] == plan.rule_log
+
+
+def test_solve_batched_singular_instance_raises():
+    n, bt = 8, 4
+    A = np.tile(np.eye(n), (bt, 1, 1)) * 3.0 + 0.1
+    A[2][:, 3] = 0.0
+    with pytest.raises(lm.SingularMatrixError):
+        solve_batched(stack_fortran(A), stack_fortran(np.ones((bt, n, 1))))
+
+
+@pytest.mark.parametrize("n", [1, 5, 32, 33, 64, 128])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_atb_schur_trace_vs_oracle(n, dtype):
+    rng = np.random.default_rng(n)
+    bt = 9
+    ops = [rng.uniform(-1, 1, (bt, n, n)) for _ in range(4)]
+    if dtype == torch.float32:
+        ops = [o.astype(np.float32).astype(np.float64) for o in ops]  # oracle on the f32-rounded inputs
+    E, s = atb_schur_trace(*(stack_fortran(o, dtype=dtype) for o in ops))
+    E, s = E.cpu().numpy(), s.cpu().numpy()
+    pops, pargs, *_ = parse_program("x0 x1 x2 * +")
+    tol = 1e-12 if dtype == torch.float64 else 1e-5
+    for i in range(bt):
+        A, B, C, D = (np.asfortranarray(o[i]) for o in ops)
+        g = np.zeros((n, n), order="F")
+        O.gemm(A.T, B, g)
+        Er = np.zeros((n, n), order="F")
+        O.program(pops.numpy(), pargs.numpy(), [], [g, C, D], Er)
+        assert np.max(np.abs(E[i] - Er)) <= tol * max(np.max(np.abs(Er)), 1e-30)
+        tr = O.trace_of_product(A, B)
+        assert abs(s[i] - tr) <= tol * max(abs(tr), np.sum(np.abs(A * B.T)) * 1e-2)
