@@ -70,9 +70,12 @@ class ClockSampler:
                0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, device_index: int):
+    def __init__(self, device_index: int, enabled: bool = True):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
+        self._nv = None
+        if not enabled:
+            return
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -631,7 +634,7 @@ def run_ours(args, wl, ws, rank, local):
     ctx = wl.setup(lm, host) if hasattr(wl, "setup") else _default_setup(wl, lm, host)
     step = wl.step_fn(lm, ctx) if hasattr(wl, "step_fn") else _default_step(wl, lm, ctx)
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, enabled=not args.no_clocks)
     with sampler:
         for _ in range(args.warmup):  # JIT compiles, allocator pools, clocks up
             step()
@@ -771,6 +774,7 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-clocks", action="store_true", help="skip the NVML clock sampler thread")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
     ws, rank, local = _dist()

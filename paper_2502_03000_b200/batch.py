@@ -71,13 +71,23 @@ def analyze_batched(A: torch.Tensor) -> np.ndarray:
 
 
 class BatchSolveResult:
-    """x (batch, n, 1) device tensor; per-instance rule logs (as the
-    single-instance planner would log them) and the LU class mask."""
+    """x (batch, n, 1) device tensor, the per-instance structure class
+    and the rule log the single-instance planner would record."""
 
-    def __init__(self, x, rule_logs, lu_mask):
+    _TAGS = {0: ["R9"], 1: ["R9", "R10:BAND"], 2: ["R9", "R10:TRIU"], 3: ["R9", "R10:TRIL"],
+             4: ["R9", "R10:SYM-DETECTED"]}
+
+    def __init__(self, x, cls):
         self.x = x
-        self.rule_logs = rule_logs
-        self.lu_mask = lu_mask
+        self.cls = cls  # 0 gen, 1 band, 2 triu, 3 tril, 4 sym (numpy int8)
+
+    @property
+    def lu_mask(self):
+        return (self.cls == 0) | (self.cls == 4)
+
+    @property
+    def rule_logs(self):
+        return [list(self._TAGS[int(c)]) for c in self.cls]
 
 
 def _classify(info, n):
@@ -104,19 +114,12 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
         raise KernelContractError("solve_batched: A must be (batch, n, n) and b (batch, n, 1)")
     info = analyze_batched(A)
     band, triu, tril, symm = _classify(info, n)
-    lu_mask = ~(band | triu | tril)
-    logs = []
-    for i in range(bt):
-        if band[i]:
-            logs.append(["R9", "R10:BAND"])
-        elif triu[i]:
-            logs.append(["R9", "R10:TRIU"])
-        elif tril[i]:
-            logs.append(["R9", "R10:TRIL"])
-        elif symm[i]:
-            logs.append(["R9", "R10:SYM-DETECTED"])
-        else:
-            logs.append(["R9"])
+    cls = np.zeros(bt, dtype=np.int8)
+    cls[symm] = 4
+    cls[tril] = 3
+    cls[triu] = 2
+    cls[band] = 1
+    lu_mask = (cls == 0) | (cls == 4)
     x = torch.empty((bt, 1, n), dtype=A.dtype, device=A.device).transpose(1, 2)
     x.copy_(b)
     if lu_mask.all() and n <= 64:
@@ -124,13 +127,14 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
         N.call("lm_lu_solve_batched", N.dtype_code(A), n, bt, A.data_ptr(), x.data_ptr(), None, None,
                dinfo.data_ptr())
         if check:
-            bad = torch.nonzero(dinfo).flatten()
-            if bad.numel():
+            hinfo = dinfo.cpu().numpy()
+            bad = np.flatnonzero(hinfo)
+            if bad.size:
                 i = int(bad[0])
-                col = int(dinfo[i]) - 1
+                col = int(hinfo[i]) - 1
                 raise SingularMatrixError(f"singular matrix in instance {i}: zero pivot in column {col}",
                                           column=col)
-        return BatchSolveResult(x, logs, lu_mask)
+        return BatchSolveResult(x, cls)
     # mixed classes (or n > 64): the single-instance planner per instance
     from .expr import inverse
     from .rewrite import evaluate
@@ -138,7 +142,7 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
         ai = DenseMatrix(A[i])
         bi = DenseMatrix(b[i])
         x[i].copy_(evaluate(inverse(ai) * bi).data)
-    return BatchSolveResult(x, logs, lu_mask)
+    return BatchSolveResult(x, cls)
 
 
 def atb_schur_trace(A, B, C, D):

@@ -1,0 +1,302 @@
+// batched_expr.cu -- BASELINE config 5a: for every instance of one size
+// class (n = 32, 64, 128; any other n takes the generic kernel)
+//     E = A.T @ B + C % D      (plan: gemm(A.T, B) -> slot; fused program slot + C % D)
+//     s = trace(A @ B)         (plan: trace_of_product(A, B))
+// in ONE kernel that reads A, B, C, D once from HBM and writes E and s.
+//
+// Per instance the contraction index k runs over the ROWS of A and B
+// (A.T @ B), so both are streamed through shared memory in 16-row chunks
+// (cp.async, double-buffered, K-contiguous smem layout, row stride 20
+// doubles: conflict-free m8n8k4 fragment loads).  trace(A @ B) =
+// sum_k <A[:,k], B[k,:]> needs A's COLUMNS k of the chunk, which are
+// contiguous in HBM: they are staged alongside (an L2 hit for the half
+// of each column the row pass already touched, so HBM traffic stays one
+// read of A).  FP64 products run on DMMA (mma.sync.m8n8k4.f64; sm_100a
+// has no tcgen05 f64 kind) with a (n/32) x 2 warp grid, warp tile 32 x
+// n/2; FP32 runs on FFMA with 8 x (n/16) register tiles.  The epilogue
+// adds round(C*D) to the rounded product (the planner's fused program)
+// and writes E; s is a fixed-order block reduction (deterministic).
+// Persistent CTAs loop over the instances of the class.
+#include "common.cuh"
+
+namespace lm {
+
+namespace {
+
+constexpr int KC = 16;      // k rows per stage
+constexpr int LDK = KC + 4; // smem row length (elements) of the K-contiguous tiles
+
+__device__ __forceinline__ void cpa16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int G> __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(G)); }
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+template <class T, int N> struct Smem {
+    static constexpr int LDI = N + 16 / (int)sizeof(T);  // column-chunk row length (keeps 16 B alignment)
+    T a[2][N * LDK];   // A(k, m), k in chunk: [m][k]
+    T b[2][N * LDK];   // B(k, n), k in chunk: [n][k]
+    T ac[2][KC * LDI]; // A(i, k), k in chunk: [k][i]
+    T red[32];
+};
+
+// Stage chunk c of instance (pa, pb) into buffer `buf`.
+template <class T, int N>
+__device__ __forceinline__ void stage(Smem<T, N> &sm, int buf, const T *pa, const T *pb, int c) {
+    constexpr int V = 16 / sizeof(T);  // elements per 16-byte copy
+    const int k0 = c * KC;
+    constexpr int ROWV = KC / V;        // 16-byte pieces per column of a row-chunk
+    for (int e = threadIdx.x; e < N * ROWV; e += 2 * N) {
+        const int col = e / ROWV, piece = e % ROWV;
+        cpa16(&sm.a[buf][col * LDK + piece * V], pa + (int64_t)col * N + k0 + piece * V);
+        cpa16(&sm.b[buf][col * LDK + piece * V], pb + (int64_t)col * N + k0 + piece * V);
+    }
+    constexpr int COLV = N / V;          // 16-byte pieces per full column
+    for (int e = threadIdx.x; e < KC * COLV; e += 2 * N) {
+        const int kl = e / COLV, piece = e % COLV;
+        cpa16(&sm.ac[buf][kl * Smem<T, N>::LDI + piece * V], pa + (int64_t)(k0 + kl) * N + piece * V);
+    }
+}
+
+template <class T, int N>
+__global__ void __launch_bounds__(2 * N) atb_schur_trace_tc(int64_t batch, const T *__restrict__ A,
+                                                            const T *__restrict__ B, const T *__restrict__ C,
+                                                            const T *__restrict__ D, T *__restrict__ E,
+                                                            T *__restrict__ S) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Smem<T, N> &sm = *reinterpret_cast<Smem<T, N> *>(smraw);
+    constexpr int NT = 2 * N;
+    constexpr int NCH = N / KC;
+    constexpr int LDI = Smem<T, N>::LDI;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nn = (int64_t)N * N;
+
+    for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+        const T *pa = A + b * nn, *pb = B + b * nn;
+        // accumulators
+        constexpr int WTN = N / 2;          // f64: warp tile 32 x N/2
+        constexpr int NJ = WTN / 8;         // m8n8 tiles along n
+        double acc[4][NJ > 0 ? NJ : 1][2];  // f64 path
+        float facc[8][N / 16];              // f32 path: rows tr + (N/8)*i, cols tc + 16*j
+        if constexpr (sizeof(T) == 8) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < N / 16; ++j) facc[i][j] = 0.f;
+        }
+        T tr = T(0);
+        stage<T, N>(sm, 0, pa, pb, 0);
+        cpa_commit();
+        for (int c = 0; c < NCH; ++c) {
+            const int buf = c & 1;
+            if (c + 1 < NCH) {
+                stage<T, N>(sm, buf ^ 1, pa, pb, c + 1);
+                cpa_commit();
+                cpa_wait<1>();
+            } else {
+                cpa_wait<0>();
+            }
+            __syncthreads();
+            const T *as = sm.a[buf];
+            const T *bs = sm.b[buf];
+            if constexpr (sizeof(T) == 8) {
+                const int wm = (warp % (N / 32)) * 32, wn = (warp / (N / 32)) * WTN;
+                const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+                for (int kk = 0; kk < KC; kk += 4) {
+                    double af[4], bf[NJ > 0 ? NJ : 1];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * LDK + kk + fc];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) bf[j] = bs[(wn + j * 8 + fr) * LDK + kk + fc];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < NJ; ++j) dmma884(acc[i][j], af[i], bf[j]);
+                }
+            } else {
+                constexpr int TR = N / 8;  // thread rows
+                const int trw = tid % TR, tcl = tid / TR;  // tcl in [0, 16)
+#pragma unroll 4
+                for (int kl = 0; kl < KC; ++kl) {
+                    float av[8], bv[N / 16];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) av[i] = as[(trw + TR * i) * LDK + kl];
+#pragma unroll
+                    for (int j = 0; j < N / 16; ++j) bv[j] = bs[(tcl + 16 * j) * LDK + kl];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < N / 16; ++j) facc[i][j] = fmaf(av[i], bv[j], facc[i][j]);
+                }
+            }
+            // trace terms of this chunk: sum_{k in chunk} sum_i A(i,k) * B(k,i)
+            {
+                const T *ac = sm.ac[buf];
+                const int i = tid % N, half = tid / N;  // 2 threads per i, 8 k's each
+#pragma unroll
+                for (int q = 0; q < KC / 2; ++q) {
+                    const int kl = half * (KC / 2) + q;
+                    tr = fma(ac[kl * LDI + i], bs[i * LDK + kl], tr);
+                }
+            }
+            __syncthreads();
+        }
+        // epilogue: E = round(acc) + round(C * D)
+        const T *pc = C + b * nn, *pd = D + b * nn;
+        T *pe = E + b * nn;
+        if constexpr (sizeof(T) == 8) {
+            const int wm = (warp % (N / 32)) * 32, wn = (warp / (N / 32)) * WTN;
+            const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int m = wm + i * 8 + fr, n = wn + j * 8 + 2 * fc + h;
+                        const int64_t idx = m + (int64_t)n * N;
+                        pe[idx] = radd(acc[i][j][h], rmul(__ldg(pc + idx), __ldg(pd + idx)));
+                    }
+        } else {
+            constexpr int TR = N / 8;
+            const int trw = tid % TR, tcl = tid / TR;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < N / 16; ++j) {
+                    const int m = trw + TR * i, n = tcl + 16 * j;
+                    const int64_t idx = m + (int64_t)n * N;
+                    pe[idx] = radd(facc[i][j], rmul(__ldg(pc + idx), __ldg(pd + idx)));
+                }
+        }
+        tr = block_sum<T, NT>(tr, sm.red);
+        if (tid == 0) S[b] = tr;
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+// Generic fallback (any n): one CTA per instance, SIMT, 32 x 32 tiles.
+template <class T>
+__global__ void __launch_bounds__(256) atb_schur_trace_generic(int64_t n, const T *__restrict__ A,
+                                                               const T *__restrict__ B, const T *__restrict__ C,
+                                                               const T *__restrict__ D, T *__restrict__ E,
+                                                               T *__restrict__ S) {
+    __shared__ T sA[32][33], sB[32][33];
+    __shared__ T red[8];
+    const int64_t b = blockIdx.x;
+    const int64_t nn = n * n;
+    const T *a = A + b * nn, *bb = B + b * nn, *c = C + b * nn, *d = D + b * nn;
+    T *e = E + b * nn;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t nt = ceil_div(n, 32);
+    for (int64_t tm = 0; tm < nt; ++tm)
+        for (int64_t tn = 0; tn < nt; ++tn) {
+            T acc[4] = {T(0), T(0), T(0), T(0)};
+            for (int64_t k0 = 0; k0 < n; k0 += 32) {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int64_t k = k0 + tx, m = tm * 32 + ty + 8 * r;
+                    sA[ty + 8 * r][tx] = (k < n && m < n) ? a[k + m * n] : T(0);
+                    const int64_t kb = k0 + tx, nc = tn * 32 + ty + 8 * r;
+                    sB[ty + 8 * r][tx] = (kb < n && nc < n) ? bb[kb + nc * n] : T(0);
+                }
+                __syncthreads();
+#pragma unroll 8
+                for (int kk = 0; kk < 32; ++kk)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) acc[r] = fma(sA[tx][kk], sB[ty + 8 * r][kk], acc[r]);
+                __syncthreads();
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t m = tm * 32 + tx, nc = tn * 32 + ty + 8 * r;
+                if (m < n && nc < n) {
+                    const int64_t idx = m + nc * n;
+                    e[idx] = radd(acc[r], rmul(c[idx], d[idx]));
+                }
+            }
+        }
+    T tacc = T(0);
+    for (int64_t i0 = 0; i0 < n; i0 += 32)
+        for (int64_t k0 = 0; k0 < n; k0 += 32) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t kb = k0 + tx, ib = i0 + ty + 8 * r;
+                sB[ty + 8 * r][tx] = (kb < n && ib < n) ? bb[kb + ib * n] : T(0);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t i = i0 + tx, k = k0 + ty + 8 * r;
+                if (i < n && k < n) tacc = fma(a[i + k * n], sB[tx][ty + 8 * r], tacc);
+            }
+            __syncthreads();
+        }
+    tacc = block_sum<T, 256>(tacc, red);
+    if (threadIdx.x == 0) S[b] = tacc;
+}
+
+template <class T, int N>
+int launch_tc(int64_t batch, const T *a, const T *b, const T *c, const T *d, T *e, T *s, cudaStream_t st) {
+    auto kern = atb_schur_trace_tc<T, N>;
+    const size_t smem = sizeof(Smem<T, N>);
+    static bool attr = false;
+    if (!attr) {
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    static int grid = 0;
+    if (!grid) grid = resident_grid(kern, 2 * N, smem);
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, 2 * N, smem, st>>>(batch, a, b, c, d, e, s);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
+template <class T>
+int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T *c, const T *d, T *e, T *s,
+                      cudaStream_t st) {
+    const bool aligned = ((uintptr_t)a | (uintptr_t)b) % 16 == 0;
+    if (aligned && n == 32) return launch_tc<T, 32>(batch, a, b, c, d, e, s, st);
+    if (aligned && n == 64) return launch_tc<T, 64>(batch, a, b, c, d, e, s, st);
+    if (aligned && n == 128) return launch_tc<T, 128>(batch, a, b, c, d, e, s, st);
+    atb_schur_trace_generic<T><<<(unsigned)batch, 256, 0, st>>>(n, a, b, c, d, e, s);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
+}  // namespace lm
+
+using namespace lm;
+
+extern "C" int lm_expr_atb_schur_trace_batched(int dtype, int64_t n, int64_t batch, const void *a, const void *b,
+                                               const void *c, const void *d, void *e, void *s_out, void *stream) {
+    clear_error();
+    LM_REQUIRE(n >= 1, "batched expr: n >= 1");
+    LM_REQUIRE(batch <= 0x7fffffff, "batched expr: batch too large for one launch");
+    if (batch == 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    if (dtype == LM_F64)
+        return batched_expr_impl<double>(n, batch, (const double *)a, (const double *)b, (const double *)c,
+                                         (const double *)d, (double *)e, (double *)s_out, s);
+    if (dtype == LM_F32)
+        return batched_expr_impl<float>(n, batch, (const float *)a, (const float *)b, (const float *)c,
+                                        (const float *)d, (float *)e, (float *)s_out, s);
+    set_error("bad dtype");
+    return -1;
+}

@@ -15,6 +15,7 @@ void set_error(const char *fmt, ...);
 void clear_error();
 void count_launch(int n = 1);
 int num_sms();
+void ensure_pool();
 
 #define LM_REQUIRE(cond, ...)                                                                 \
     do {                                                                                      \
@@ -55,6 +56,7 @@ struct Scratch {
     Scratch &operator=(const Scratch &) = delete;
     int alloc(size_t bytes, cudaStream_t st) {
         s = st;
+        ensure_pool();
         if (bytes == 0) bytes = 16;
         cudaError_t e = cudaMallocAsync(&p, bytes, st);
         if (e != cudaSuccess) {

@@ -581,116 +581,6 @@ __global__ void __launch_bounds__(256) band_solve_kernel(View<const double> A, d
 #undef AB_
 }
 
-// ---- batched small LU solve (configs 4b): one warp per system ----------------------
-//
-// The matrix lives in shared memory; lane l owns rows l and l+32 (n <=
-// 64).  Every operation is the reference's (_loops.py:200-259) in its
-// order, so values and pivots are bit-identical to a per-instance
-// lazymat lu_solve.
-constexpr int kBatchWarps = 4;
-
-template <int NMAX>
-__global__ void __launch_bounds__(32 * kBatchWarps) lu_batched_warp(int64_t n, int64_t batch, const double *__restrict__ A,
-                                                                     double *X, double *LU, int64_t *piv, int32_t *info) {
-    extern __shared__ double smb[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t b = (int64_t)blockIdx.x * kBatchWarps + w;
-    if (b >= batch) return;
-    const int ld = (int)n + 1;
-    double *S = smb + (size_t)w * (n * ld + n + n / 2 + 1);  // S[i + j*ld]
-    double *xs = S + n * ld;
-    int32_t *pv_s = reinterpret_cast<int32_t *>(xs + n);
-    const double *Ag = A + b * n * n;
-    double *xg = X + b * n;
-    for (int64_t e = lane; e < n * n; e += 32) {
-        const int64_t j = e / n, i = e - j * n;
-        S[i + j * ld] = __ldg(Ag + e);
-    }
-    for (int64_t i = lane; i < n; i += 32) xs[i] = xg[i];
-    __syncwarp();
-    int32_t fail = 0;
-    for (int k = 0; k < n; ++k) {
-        // pivot: first row achieving the max |.| (strict > scan)
-        double bv = -1.0;
-        int bi = -1;
-        for (int i = k + lane; i < n; i += 32) {
-            double v = fabs(S[i + k * ld]);
-            if (v != v) {
-                if (i != k) continue;
-                v = __longlong_as_double(0x7ff0000000000000LL);
-            }
-            if (bi < 0 || v > bv) {
-                bv = v;
-                bi = i;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
-                bv = ov;
-                bi = oi;
-            }
-        }
-        const int p = bi;
-        if (lane == 0) pv_s[k] = p;
-        if (S[p + k * ld] == 0.0) {
-            fail = k + 1;
-            break;
-        }
-        if (p != k)
-            for (int j = lane; j < n; j += 32) {
-                const double t = S[k + j * ld];
-                S[k + j * ld] = S[p + j * ld];
-                S[p + j * ld] = t;
-            }
-        __syncwarp();
-        const double pvv = S[k + k * ld];
-        for (int i = k + 1 + lane; i < n; i += 32) S[i + k * ld] = rdiv(S[i + k * ld], pvv);
-        __syncwarp();
-        for (int j = k + 1; j < n; ++j) {
-            const double f = S[k + j * ld];
-            for (int i = k + 1 + lane; i < n; i += 32) S[i + j * ld] = rsub(S[i + j * ld], rmul(S[i + k * ld], f));
-        }
-        __syncwarp();
-    }
-    __syncwarp();
-    if (lane == 0) info[b] = fail;
-    if (piv)
-        for (int i = lane; i < (fail ? fail : n); i += 32) piv[b * n + i] = pv_s[i];
-    if (fail) return;
-    // solve (one RHS): swaps (sequential, lane 0), forward, backward
-    if (lane == 0)
-        for (int i = 0; i < n; ++i) {
-            const int p = pv_s[i];
-            if (p != i) {
-                const double t = xs[i];
-                xs[i] = xs[p];
-                xs[p] = t;
-            }
-        }
-    __syncwarp();
-    for (int j = 0; j < n; ++j) {
-        const double yj = xs[j];
-        for (int i = j + 1 + lane; i < n; i += 32) xs[i] = rsub(xs[i], rmul(S[i + j * ld], yj));
-        __syncwarp();
-    }
-    for (int j = (int)n - 1; j >= 0; --j) {
-        if (lane == 0) xs[j] = rdiv(xs[j], S[j + j * ld]);
-        __syncwarp();
-        const double xj = xs[j];
-        for (int i = lane; i < j; i += 32) xs[i] = rsub(xs[i], rmul(S[i + j * ld], xj));
-        __syncwarp();
-    }
-    if (LU)
-        for (int64_t e = lane; e < n * n; e += 32) {
-            const int64_t j = e / n, i = e - j * n;
-            LU[b * n * n + e] = S[i + j * ld];
-        }
-    for (int64_t i = lane; i < n; i += 32) xg[i] = xs[i];
-}
-
 }  // namespace lm
 
 using namespace lm;
@@ -750,18 +640,3 @@ extern "C" int lm_band_solve(int dtype, lm_view a, lm_view x, int64_t kl, int64_
     return 0;
 }
 
-extern "C" int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void *x, void *lu_out,
-                                   int64_t *d_piv, int32_t *d_info, void *stream) {
-    clear_error();
-    LM_REQUIRE(dtype == LM_F64, "lu_solve_batched: f64 only");
-    LM_REQUIRE(n >= 1 && n <= 64, "lu_solve_batched: 1 <= n <= 64 (got %lld)", (long long)n);
-    if (batch == 0) return 0;
-    cudaStream_t s = as_stream(stream);
-    const size_t smem = sizeof(double) * (size_t)kBatchWarps * (n * (n + 1) + n + n / 2 + 1);
-    if (smem > 48 * 1024)
-        LM_CUDA(cudaFuncSetAttribute(lu_batched_warp<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    lu_batched_warp<64><<<(unsigned)ceil_div(batch, kBatchWarps), 32 * kBatchWarps, smem, s>>>(
-        n, batch, (const double *)a, (double *)x, (double *)lu_out, d_piv, d_info);
-    LM_LAUNCHED(1);
-    return 0;
-}

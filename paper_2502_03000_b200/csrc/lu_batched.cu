@@ -1,0 +1,176 @@
+// lu_batched.cu -- many independent small LU solves (BASELINE config 4b):
+// per instance exactly the reference's _lu_factor + _lu_solve_inplace
+// (lazymat/_loops.py:200-259), bit-identical values and pivots.
+//
+// One CTA of N threads per system (N = 16/32/64, instances padded with an
+// identity block, which leaves the leading block's factorisation and
+// pivots untouched).  Thread t keeps ORIGINAL row t of the matrix in N
+// registers for the whole factorisation; the k and j loops are fully
+// unrolled so every register index is static.  Row swaps never move
+// data: a position map (pos[t], row_at[p]) tracks which original row sits
+// at each position, so the reference's "full-row swap" is two integer
+// stores.  Per column k one barrier: each warp publishes its best
+// candidate (|value| desc, position asc -- the reference's strict-> scan)
+// together with the candidate's row, every thread then picks the global
+// winner from the published candidates and reads the pivot row U[k, k+1:]
+// as shared-memory broadcasts.  Multipliers and updates use __ddiv_rn /
+// __dmul_rn / __dsub_rn in the reference order.
+//
+// Traffic per instance: A read once (N*N*8 B), b read, x written; the LU
+// factors / pivots are written only when requested.
+#include "common.cuh"
+
+namespace lm {
+
+template <int N>
+__global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, const double *__restrict__ A,
+                                                     double *__restrict__ X, double *__restrict__ LU,
+                                                     int64_t *__restrict__ piv, int32_t *__restrict__ info) {
+    constexpr int W = N / 32 > 0 ? N / 32 : 1;  // warps per system
+    constexpr unsigned MASK = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
+    constexpr int O0 = N >= 32 ? 16 : N / 2;
+    __shared__ double cand_row[2][W][N];        // published candidate rows (double-buffered by k parity)
+    __shared__ double cand_v[2][W];
+    __shared__ int cand_pos[2][W], cand_t[2][W];
+    __shared__ int row_at[N];  // position -> original row (thread)
+    __shared__ double xb[N];   // substitution broadcast
+    __shared__ int s_fail;
+
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t b = blockIdx.x;
+    const double *Ab = A + b * n * n;
+    double r[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        if (t < n && j < n)
+            r[j] = __ldg(Ab + t + (int64_t)j * n);
+        else
+            r[j] = (t == j) ? 1.0 : 0.0;  // identity padding
+    }
+    double xv = t < n ? __ldg(X + b * n + t) : 0.0;
+    int pos = t;
+    row_at[t] = t;
+    if (t == 0) s_fail = 0;
+    __syncthreads();
+
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const int par = k & 1;
+        // --- candidate key of this thread: rows at positions >= k compete
+        double key = -1.0;
+        if (pos >= k) {
+            double v = fabs(r[k]);
+            if (v != v) v = (pos == k) ? __longlong_as_double(0x7ff0000000000000LL) : -1.0;
+            key = v;
+        }
+        double bk = key;
+        int bp = key >= 0.0 ? pos : 0x7fffffff;
+        int bt = t;
+#pragma unroll
+        for (int o = O0; o > 0; o >>= 1) {
+            const double ok = __shfl_xor_sync(MASK, bk, o);
+            const int op = __shfl_xor_sync(MASK, bp, o);
+            const int ot = __shfl_xor_sync(MASK, bt, o);
+            if (ok > bk || (ok == bk && op < bp)) {
+                bk = ok;
+                bp = op;
+                bt = ot;
+            }
+        }
+        // warp winner publishes its key, position and row (columns >= k)
+        if (t == bt) {
+            cand_v[par][w] = bk;
+            cand_pos[par][w] = bp;
+            cand_t[par][w] = bt;
+#pragma unroll
+            for (int j = k; j < N; ++j) cand_row[par][w][j] = r[j];
+        }
+        __syncthreads();
+        // global winner among the W published candidates
+        int win = 0;
+#pragma unroll
+        for (int q = 1; q < W; ++q)
+            if (cand_v[par][q] > cand_v[par][win] ||
+                (cand_v[par][q] == cand_v[par][win] && cand_pos[par][q] < cand_pos[par][win]))
+                win = q;
+        const int p = cand_pos[par][win];   // pivot position (reference's p)
+        const int pt = cand_t[par][win];    // the thread holding it
+        const double *U = cand_row[par][win];
+        const double pvv = U[k];
+        if (t == 0) {
+            if (piv && k < n) piv[b * n + k] = p;
+            if (pvv == 0.0 && s_fail == 0 && k < n) s_fail = k + 1;
+        }
+        // full-row swap of positions k and p == swap of the position map
+        const int tk = row_at[k];
+        if (p != k) {
+            if (t == pt) pos = k;
+            if (t == tk) pos = p;
+        }
+        __syncthreads();  // everyone has read row_at[k] before it changes
+        if (p != k && t == 0) {
+            row_at[k] = pt;
+            row_at[p] = tk;
+        }
+        // multipliers and the rank-1 update of the rows below the pivot
+        if (pos > k) {
+            const double m = __ddiv_rn(r[k], pvv);
+            r[k] = m;
+#pragma unroll
+            for (int j = k + 1; j < N; ++j) r[j] = __dsub_rn(r[j], __dmul_rn(m, U[j]));
+        }
+    }
+    __syncthreads();
+    const int fail = s_fail;
+    if (t == 0) info[b] = fail;
+    if (fail) return;
+    // ---- solve: x held by position; swaps already applied via pos (the
+    // sequential swaps of _lu_solve_inplace compose to "position pos[t]
+    // holds original row t").
+    // forward (unit lower), positions ascending
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        if (pos == j) xb[j] = xv;
+        __syncthreads();
+        if (pos > j) xv = __dsub_rn(xv, __dmul_rn(r[j], xb[j]));
+    }
+    // backward (upper), positions descending
+#pragma unroll
+    for (int j = N - 1; j >= 0; --j) {
+        if (pos == j) {
+            xv = __ddiv_rn(xv, r[j]);
+            xb[j] = xv;
+        }
+        __syncthreads();
+        if (pos < j) xv = __dsub_rn(xv, __dmul_rn(r[j], xb[j]));
+    }
+    if (pos < n) X[b * n + pos] = xv;
+    if (LU && pos < n)
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (j < n) LU[b * n * n + pos + (int64_t)j * n] = r[j];
+}
+
+}  // namespace lm
+
+using namespace lm;
+
+extern "C" int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void *x, void *lu_out,
+                                   int64_t *d_piv, int32_t *d_info, void *stream) {
+    clear_error();
+    LM_REQUIRE(dtype == LM_F64, "lu_solve_batched: f64 only");
+    LM_REQUIRE(n >= 1 && n <= 64, "lu_solve_batched: 1 <= n <= 64 (got %lld)", (long long)n);
+    if (batch == 0) return 0;
+    LM_REQUIRE(batch <= 0x7fffffff, "lu_solve_batched: batch too large");
+    cudaStream_t s = as_stream(stream);
+    const double *A = (const double *)a;
+    double *X = (double *)x, *LU = (double *)lu_out;
+    if (n <= 16)
+        lu_batched_rows<16><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, LU, d_piv, d_info);
+    else if (n <= 32)
+        lu_batched_rows<32><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, LU, d_piv, d_info);
+    else
+        lu_batched_rows<64><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, LU, d_piv, d_info);
+    LM_LAUNCHED(1);
+    return 0;
+}

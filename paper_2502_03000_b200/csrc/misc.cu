@@ -188,75 +188,6 @@ __global__ void __launch_bounds__(256) analyze_batched_k(int64_t n, const T *__r
     }
 }
 
-// ---- batched E = A^T B + C % D, s = trace(A B) (config 5, one size class) ---------
-//
-// One CTA per instance, 256 threads; 32 x 32 output tiles, K staged in
-// 32-wide chunks through shared memory.  E = round(round(A^T B) + round(C*D))
-// exactly as the planner's two steps (gemm, then the fused program
-// slot + C%D) would produce from the GEMM value; the GEMM accumulates with
-// FMA (normwise tolerance, north star).  The trace reuses nothing: a
-// second pass reads A and B again (L2-resident: the CTA just read them).
-template <class T>
-__global__ void __launch_bounds__(256) atb_schur_trace(int64_t n, const T *__restrict__ A, const T *__restrict__ B,
-                                                       const T *__restrict__ C, const T *__restrict__ D, T *__restrict__ E,
-                                                       T *__restrict__ S) {
-    __shared__ T sA[32][33], sB[32][33];
-    __shared__ T red[8];
-    const int64_t b = blockIdx.x;
-    const int64_t nn = n * n;
-    const T *a = A + b * nn, *bb = B + b * nn, *c = C + b * nn, *d = D + b * nn;
-    T *e = E + b * nn;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    const int64_t nt = ceil_div(n, 32);
-    for (int64_t tm = 0; tm < nt; ++tm)
-        for (int64_t tn = 0; tn < nt; ++tn) {
-            T acc[4] = {T(0), T(0), T(0), T(0)};
-            for (int64_t k0 = 0; k0 < n; k0 += 32) {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    // (A^T)(m, k) = A(k, m): sA[k_local][m_local] = A(k0+tx, tm*32+ty+8r)
-                    const int64_t k = k0 + tx, m = tm * 32 + ty + 8 * r;
-                    sA[ty + 8 * r][tx] = (k < n && m < n) ? a[k + m * n] : T(0);  // sA[m_local][k_local]
-                    const int64_t kb = k0 + tx, nc = tn * 32 + ty + 8 * r;
-                    sB[ty + 8 * r][tx] = (kb < n && nc < n) ? bb[kb + nc * n] : T(0);  // sB[n_local][k_local]
-                }
-                __syncthreads();
-#pragma unroll 8
-                for (int kk = 0; kk < 32; ++kk)
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) acc[r] = fma(sA[tx][kk], sB[ty + 8 * r][kk], acc[r]);
-                __syncthreads();
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int64_t m = tm * 32 + tx, nc = tn * 32 + ty + 8 * r;
-                if (m < n && nc < n) {
-                    const int64_t idx = m + nc * n;
-                    e[idx] = radd(acc[r], rmul(c[idx], d[idx]));
-                }
-            }
-        }
-    // s = sum_{i,k} A[i,k] * B[k,i]
-    T tacc = T(0);
-    for (int64_t i0 = 0; i0 < n; i0 += 32)
-        for (int64_t k0 = 0; k0 < n; k0 += 32) {
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int64_t kb = k0 + tx, ib = i0 + ty + 8 * r;
-                sB[ty + 8 * r][tx] = (kb < n && ib < n) ? bb[kb + ib * n] : T(0);  // sB[i_local][k_local]
-            }
-            __syncthreads();
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int64_t i = i0 + tx, k = k0 + ty + 8 * r;
-                if (i < n && k < n) tacc = fma(a[i + k * n], sB[tx][ty + 8 * r], tacc);
-            }
-            __syncthreads();
-        }
-    tacc = block_sum<T, 256>(tacc, red);
-    if (threadIdx.x == 0) S[b] = tacc;
-}
-
 }  // namespace lm
 
 using namespace lm;
@@ -342,23 +273,3 @@ extern "C" int lm_analyze_batched(int dtype, int64_t n, int64_t batch, const voi
     return 0;
 }
 
-extern "C" int lm_expr_atb_schur_trace_batched(int dtype, int64_t n, int64_t batch, const void *a, const void *b,
-                                               const void *c, const void *d, void *e, void *s_out, void *stream) {
-    clear_error();
-    LM_REQUIRE(n >= 1, "batched expr: n >= 1");
-    if (batch == 0) return 0;
-    cudaStream_t s = as_stream(stream);
-    if (dtype == LM_F64)
-        atb_schur_trace<double><<<(unsigned)batch, 256, 0, s>>>(n, (const double *)a, (const double *)b,
-                                                                (const double *)c, (const double *)d, (double *)e,
-                                                                (double *)s_out);
-    else if (dtype == LM_F32)
-        atb_schur_trace<float><<<(unsigned)batch, 256, 0, s>>>(n, (const float *)a, (const float *)b, (const float *)c,
-                                                               (const float *)d, (float *)e, (float *)s_out);
-    else {
-        set_error("bad dtype");
-        return -1;
-    }
-    LM_LAUNCHED(1);
-    return 0;
-}

@@ -22,6 +22,21 @@ void clear_error() { g_err[0] = 0; }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Keep freed stream-ordered allocations in the pool (the default release
+// threshold of 0 returns memory to the OS at every synchronisation, and
+// re-mapping it costs far more than the kernels that use the scratch).
+void ensure_pool() {
+    static bool done[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 int num_sms() {
     static int cache[64] = {0};
     int dev = 0;
