@@ -159,6 +159,13 @@ int lm_analyze_batched(int dtype, int64_t n, int64_t batch, const void *a, int64
 int lm_expr_atb_schur_trace_batched(int dtype, int64_t n, int64_t batch, const void *a, const void *b,
                                     const void *c, const void *d, void *e, void *s, void *stream);
 
+/* ---- synthetic data (bench / tests only) ------------------------------- */
+/* out(i,j) = U(lo,hi) from a counter-based hash of the GLOBAL index
+ * (row0+i, col0+j) of a matrix with global_rows rows: any slice of a
+ * distributed matrix can be generated consistently on any rank. */
+int lm_fill_uniform(int dtype, lm_view out, uint64_t seed, int64_t row0, int64_t col0, int64_t global_rows,
+                    double lo, double hi, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -257,6 +257,48 @@ extern "C" int lm_set_identity(int dtype, lm_view out, void *stream) {
     return 0;
 }
 
+// ---- synthetic data: U(lo, hi) from a counter-based hash of GLOBAL (i, j) ----
+// Any rank can generate any slice of a distributed matrix consistently
+// (config 5b: rank g needs rows of B and a column block of B).  Not on the
+// evaluation path; bench/test data only.
+namespace lm {
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+template <class T>
+__global__ void fill_hash_uniform(View<T> o, uint64_t seed, int64_t row0, int64_t col0, int64_t gld, double lo,
+                                  double hi) {
+    const int64_t n = o.rows * o.cols, nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += nth) {
+        const int64_t j = e / o.rows, i = e - j * o.rows;
+        const uint64_t g = (uint64_t)(row0 + i) + (uint64_t)(col0 + j) * (uint64_t)gld;
+        const double u = (double)(mix64(seed ^ mix64(g)) >> 11) * (1.0 / 9007199254740992.0);
+        o(i, j) = (T)(lo + (hi - lo) * u);
+    }
+}
+}  // namespace lm
+
+extern "C" int lm_fill_uniform(int dtype, lm_view out, uint64_t seed, int64_t row0, int64_t col0, int64_t global_rows,
+                               double lo, double hi, void *stream) {
+    clear_error();
+    const int64_t n = out.rows * out.cols;
+    if (n == 0) return 0;
+    cudaStream_t s = as_stream(stream);
+    if (dtype == LM_F64)
+        fill_hash_uniform<double><<<ew_grid(n), 256, 0, s>>>(to_view<double>(out), seed, row0, col0, global_rows, lo, hi);
+    else if (dtype == LM_F32)
+        fill_hash_uniform<float><<<ew_grid(n), 256, 0, s>>>(to_view<float>(out), seed, row0, col0, global_rows, lo, hi);
+    else {
+        set_error("bad dtype");
+        return -1;
+    }
+    LM_LAUNCHED(1);
+    return 0;
+}
+
 extern "C" int lm_analyze_batched(int dtype, int64_t n, int64_t batch, const void *a, int64_t *d_out, void *stream) {
     clear_error();
     if (batch == 0) return 0;

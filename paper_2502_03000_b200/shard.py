@@ -1,0 +1,85 @@
+"""Row-sharded multi-GPU evaluation (BASELINE config 5b).
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).
+For an n x n problem, rank g of G owns rows [lo_g, hi_g) of every
+operand (``row_range``: contiguous, balanced):
+
+* element-wise expressions (the config-1 program) are row-local -- each
+  rank evaluates its row block through the normal planner/kernels, no
+  communication at all;
+* trace(A*B) = sum_g sum_{i in rows_g} sum_k A[i,k] B[k,i]: rank g needs
+  its row block of A and the matching COLUMN block of B, computes the
+  partial with the same trace_of_product kernel (it accepts p x q / q x p
+  operands, lazymat/kernels.py:157-164), and one NCCL all-reduce of a
+  single float64 finishes it -- the only collective, because it is the
+  only real exchange step.
+
+The partial-trace function is injectable so the host-side sharding and
+reduction logic is testable on CPU with the gloo backend
+(tests/test_shard.py); the product path always uses the CUDA kernel.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import kernels
+from .matrix import DenseMatrix
+
+__all__ = ["row_range", "ShardedTrace", "eval_rows", "fill_uniform"]
+
+
+def row_range(n: int, rank: int, world: int) -> tuple:
+    """Contiguous balanced row block [lo, hi) of rank ``rank``."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _device_partial(a_rows: torch.Tensor, b_cols: torch.Tensor, out: torch.Tensor) -> None:
+    kernels.trace_of_product(a_rows, b_cols, out=out)
+
+
+class ShardedTrace:
+    """trace(A @ B) over row shards: local partial + one all-reduce."""
+
+    def __init__(self, group=None, partial_fn=None):
+        self.group = group
+        self.partial_fn = partial_fn or _device_partial
+
+    def __call__(self, a_rows: torch.Tensor, b_cols: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+        """a_rows: (R, n) row block of A; b_cols: (n, R) matching column
+        block of B.  Returns the 1-element tensor holding the GLOBAL trace
+        (on every rank)."""
+        if out is None:
+            out = torch.empty(1, dtype=a_rows.dtype, device=a_rows.device)
+        self.partial_fn(a_rows, b_cols, out)
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
+        return out
+
+
+def fill_uniform(t: torch.Tensor, seed: int, row0: int = 0, col0: int = 0, global_rows: int = None,
+                 lo: float = -1.0, hi: float = 1.0) -> torch.Tensor:
+    """Fill a device view with U(lo, hi) values that depend only on the
+    GLOBAL element index (row0+i, col0+j): every rank generates its slices
+    of one consistent distributed matrix (lm_fill_uniform)."""
+    from . import _native as N
+    if global_rows is None:
+        global_rows = t.shape[0]
+    N.call("lm_fill_uniform", N.dtype_code(t), N.view(t), int(seed) & 0xFFFFFFFFFFFFFFFF, int(row0), int(col0),
+           int(global_rows), float(lo), float(hi))
+    return t
+
+
+def eval_rows(build, blocks: dict, lm_module=None):
+    """Evaluate a row-local expression on this rank's row blocks through
+    the ordinary planner: ``build(lm, mats)`` returns the tree; ``blocks``
+    maps names to (R, n) device tensors (F-order)."""
+    if lm_module is None:
+        import paper_2502_03000_b200 as lm_module
+    mats = {k: DenseMatrix(v) for k, v in blocks.items()}
+    return lm_module.evaluate(build(lm_module, mats))
