@@ -345,9 +345,19 @@ int launch_trsm(const double *T, int64_t ldt, double *X, int64_t ldx, int nbj, i
 
 constexpr int kLuNb = 64;
 
+int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s);
+template <bool DESC, bool SKIP_ZERO>
+int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
+                 int64_t N, int K, cudaStream_t s);
+template <bool LOWER>
+int tri32(const double *T, int64_t ldt, double *X, int64_t ldx, int nb, int64_t ncols, cudaStream_t s);
+
 int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
     LM_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     if (n == 0) return 0;
+    // two-level blocked LU with a thread-block-cluster panel (lu_fast.cu);
+    // returns 1 when the panel does not fit a cluster -> cooperative path
+    if (int rc = lu_factor_fast(A, n, lda, piv, info, s); rc != 1) return rc;
     const int nsm = num_sms();
     Scratch pub;
     const int maxP = nsm;
@@ -424,20 +434,22 @@ int lu_solve_impl(const double *LU, int64_t n, int64_t lda, const int64_t *piv, 
         LM_CUDA(cudaMemcpyAsync(tmp.as<double>() + c * n, X + c * ldx, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     gather_rows<<<(unsigned)ceil_div(n * m, 256), 256, 0, s>>>(tmp.as<double>(), n, perm.as<int32_t>(), n, m, X, ldx);
     LM_LAUNCHED(1);
-    // 2. forward, unit lower: block J, then rows below
-    for (int64_t j0 = 0; j0 < n; j0 += kSolveNb) {
-        const int nbj = (int)((n - j0) < kSolveNb ? (n - j0) : kSolveNb);
-        if (int rc = launch_trsm<true, false>(LU + j0 + j0 * lda, lda, X + j0, ldx, nbj, m, s)) return rc;
+    // 2. forward, unit lower: 32-row block (one thread per rhs column), then
+    //    the rows below (order-preserving update, k ascending)
+    constexpr int SB = 32;
+    for (int64_t j0 = 0; j0 < n; j0 += SB) {
+        const int nbj = (int)((n - j0) < SB ? (n - j0) : SB);
+        if (int rc = tri32<true>(LU + j0 + j0 * lda, lda, X + j0, ldx, nbj, m, s)) return rc;
         const int64_t j1 = j0 + nbj;
-        if (int rc = launch_update<false, false>(LU + j1 + j0 * lda, lda, X + j0, ldx, X + j1, ldx, n - j1, m, nbj, s))
+        if (int rc = exact_update<false, false>(LU + j1 + j0 * lda, lda, X + j0, ldx, X + j1, ldx, n - j1, m, nbj, s))
             return rc;
     }
-    // 3. backward, upper: blocks from the bottom, then rows above (descending k)
-    for (int64_t jend = n; jend > 0; jend -= kSolveNb) {
-        const int64_t j0 = jend > kSolveNb ? jend - kSolveNb : 0;
+    // 3. backward, upper: blocks from the bottom, then rows above (k descending)
+    for (int64_t jend = n; jend > 0; jend -= SB) {
+        const int64_t j0 = jend > SB ? jend - SB : 0;
         const int nbj = (int)(jend - j0);
-        if (int rc = launch_trsm<false, false>(LU + j0 + j0 * lda, lda, X + j0, ldx, nbj, m, s)) return rc;
-        if (int rc = launch_update<true, false>(LU + j0 * lda, lda, X + j0, ldx, X, ldx, j0, m, nbj, s)) return rc;
+        if (int rc = tri32<false>(LU + j0 + j0 * lda, lda, X + j0, ldx, nbj, m, s)) return rc;
+        if (int rc = exact_update<true, false>(LU + j0 * lda, lda, X + j0, ldx, X, ldx, j0, m, nbj, s)) return rc;
     }
     return 0;
 }

@@ -311,3 +311,44 @@ def test_explicit_inverse_matches_solve_against_identity():
     out = fortran_empty(n, n, device=DEV)
     K.explicit_inverse_into(_strided(a), out)
     assert bits_equal(host(out), ref)
+
+
+@pytest.mark.parametrize("n", [700, 1500])
+def test_lu_factor_large_general_bitwise(n):
+    """Multi-CTA cluster panels, outer blocks and laswp: still the
+    reference's exact values and pivots on a general (pivoting) matrix."""
+    rng = np.random.default_rng(n + 1)
+    a = np.asfortranarray(rng.uniform(-1, 1, (n, n)))
+    rc, lu_ref, piv_ref = O.lu_factor(a)
+    assert rc == 0
+    lu, piv = K.lu_factor(dev(a))
+    assert np.array_equal(host(piv), piv_ref)
+    assert bits_equal(host(lu.data), lu_ref)
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, 5)))
+    x_ref = np.array(b, order="F")
+    O.lu_solve(lu_ref, piv_ref, x_ref)
+    x = dev(np.array(b, order="F"))
+    N_ = lm.kernels
+    N_.lu_solve_into(dev(a), x)
+    assert bits_equal(host(x), x_ref)
+
+
+@pytest.mark.slow
+def test_config4a_full_size_residual_and_pivots():
+    """BASELINE config 4a at full size: A = U(-1,1) + 8192 I, b 8192 x 64."""
+    n, k = 8192, 64
+    rng = np.random.default_rng(1000003 * 42 + 101 * 4)
+    a = rng.uniform(-1, 1, (n, n))
+    a[np.diag_indices(n)] += n
+    a = np.asfortranarray(a)
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, k)))
+    A = lm.DenseMatrix(a)
+    B = lm.DenseMatrix(b)
+    plan = lm.rewrite(lm.inverse(A) * B)
+    assert plan.rule_log == ["R9"] and [s.kernel for s in plan.steps] == ["lu_solve"]
+    x = lm.execute(plan).to_numpy()
+    resid = np.linalg.norm(a @ x - b, np.inf)
+    bound = 1e-10 * (np.linalg.norm(a, np.inf) * np.linalg.norm(x, np.inf) + np.linalg.norm(b, np.inf))
+    assert resid <= bound
+    _, piv = K.lu_factor(A.data)
+    assert np.array_equal(host(piv), np.arange(n))  # dominant diagonal: the reference never swaps
