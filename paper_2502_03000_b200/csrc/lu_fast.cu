@@ -9,18 +9,20 @@
 // keeps, per element, the update order k ascending performs exactly these
 // operations, so values and pivots are bit-identical to the reference.
 //
-//   outer blocks of NB = 128 columns (trailing-update K = 128: the A22
+//   outer blocks of ONB = 128 columns (trailing-update K = 128: the A22
 //   read/write traffic is n^3/(3*128) * 16 B, 23 GB at n = 8192);
 //   inside a block, panels of 32 columns factored by ONE thread-block
-//   CLUSTER (16 CTAs, one per SM of a GPC): the panel rows live in the
-//   cluster's shared memory, each column costs one cluster barrier -- the
-//   candidates and the candidate rows are published in shared-memory
-//   mailboxes before it and read over DSMEM after it;
+//   CLUSTER (up to 16 CTAs of one GPC): every thread keeps one (or two)
+//   panel rows in registers, each column costs one cluster barrier plus
+//   two DSMEM round trips -- candidates and candidate rows are published
+//   in shared-memory mailboxes before the barrier (measured on the B200:
+//   cluster barrier 0.25 us, + DSMEM round 0.2 us; a grid barrier 1.2 us);
 //   row swaps of the other columns: one composed permutation per panel
 //   (laswp_plan) applied as a gather (laswp_apply);
-//   U12: 32-row triangular solves (one thread per column, the column in
-//   registers, the triangle in shared memory) + order-preserving updates;
-//   A22: order-preserving SIMT update, 128 x 128 tiles, 8 x 8 per thread.
+//   U12: 32-row triangular solves (smem-staged columns, one thread per
+//   column) + order-preserving updates;
+//   A22: order-preserving SIMT update, 128 x 128 tiles, 8 x 8 per thread,
+//   next K chunk prefetched into registers.
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -44,6 +46,24 @@ __global__ void __launch_bounds__(256) exact_update128(const double *__restrict_
     double *sB = su + UK * ULD;  // [UK][ULD]: sB[kk][cc] = B[k, c0+cc]
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
     const int64_t i0 = (int64_t)blockIdx.x * UT, c0 = (int64_t)blockIdx.y * UT;
+    const int nch = (K + UK - 1) / UK;
+    // staging registers: 16 elements of the A chunk, 16 of the B chunk
+    double pa[16], pb[16];
+    auto fetch = [&](int q) {
+        const int k0 = (DESC ? (nch - 1 - q) : q) * UK;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int e = threadIdx.x + 256 * u;
+            const int ii = e % UT, kk = e / UT;
+            const int64_t i = i0 + ii;
+            const int k = k0 + kk;
+            pa[u] = (i < M && k < K) ? __ldg(A + i + (int64_t)k * lda) : 0.0;
+            const int kb = e % UK, cc = e / UK;
+            const int64_t c = c0 + cc;
+            pb[u] = (c < N && k0 + kb < K) ? __ldg(B + (k0 + kb) + c * ldb) : 0.0;
+        }
+    };
+    fetch(0);
     double acc[8][8];
 #pragma unroll
     for (int r = 0; r < 8; ++r)
@@ -52,23 +72,16 @@ __global__ void __launch_bounds__(256) exact_update128(const double *__restrict_
             const int64_t i = i0 + tx + 16 * r, c = c0 + ty + 16 * s;
             acc[r][s] = (i < M && c < N) ? C[i + c * ldc] : 0.0;
         }
-    const int nch = (K + UK - 1) / UK;
     for (int q = 0; q < nch; ++q) {
-        const int ch = DESC ? (nch - 1 - q) : q;
-        const int k0 = ch * UK;
-        for (int e = threadIdx.x; e < UK * UT; e += 256) {
-            const int ii = e % UT, kk = e / UT;
-            const int64_t i = i0 + ii;
-            const int k = k0 + kk;
-            sA[kk * ULD + ii] = (i < M && k < K) ? A[i + (int64_t)k * lda] : 0.0;
-        }
-        for (int e = threadIdx.x; e < UK * UT; e += 256) {
-            const int kk = e % UK, cc = e / UK;
-            const int64_t c = c0 + cc;
-            const int k = k0 + kk;
-            sB[kk * ULD + cc] = (c < N && k < K) ? B[k + c * ldb] : 0.0;
+        const int k0 = (DESC ? (nch - 1 - q) : q) * UK;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int e = threadIdx.x + 256 * u;
+            sA[(e / UT) * ULD + e % UT] = pa[u];
+            sB[(e % UK) * ULD + e / UK] = pb[u];
         }
         __syncthreads();
+        if (q + 1 < nch) fetch(q + 1);
         const int kend = (K - k0) < UK ? (K - k0) : UK;
         for (int t = 0; t < kend; ++t) {
             const int kk = DESC ? (kend - 1 - t) : t;
@@ -111,31 +124,38 @@ int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, dou
     return 0;
 }
 
-// explicit instantiations used by lu.cu (solves)
 template int exact_update<false, false>(const double *, int64_t, const double *, int64_t, double *, int64_t,
                                         int64_t, int64_t, int, cudaStream_t);
 template int exact_update<true, false>(const double *, int64_t, const double *, int64_t, double *, int64_t,
                                        int64_t, int64_t, int, cudaStream_t);
 
 // ============================================================================
-// triangular solve on up to 32 rows, one thread per column of X
+// triangular solve on up to 32 rows: columns staged through shared
+// memory (coalesced), one thread per column solves from registers
 // ============================================================================
 
+constexpr int TC = 64;  // columns per CTA
+
 template <bool LOWER>
-__global__ void __launch_bounds__(128) tri_cols(const double *__restrict__ T, int64_t ldt, double *X, int64_t ldx,
-                                                int nb, int64_t ncols) {
+__global__ void __launch_bounds__(TC) tri_cols(const double *__restrict__ T, int64_t ldt, double *X, int64_t ldx,
+                                               int nb, int64_t ncols) {
     __shared__ double sT[32][33];  // sT[i][j] = T[i,j]
-    for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    __shared__ double sX[TC][33];  // sX[c][i] = X[i, col0 + c]
+    const int64_t col0 = (int64_t)blockIdx.x * TC;
+    const int ncl = (int)((ncols - col0) < TC ? (ncols - col0) : TC);
+    for (int e = threadIdx.x; e < nb * nb; e += TC) {
         const int i = e % nb, j = e / nb;
         sT[i][j] = T[i + (int64_t)j * ldt];
     }
+    for (int e = threadIdx.x; e < nb * ncl; e += TC) {
+        const int i = e % nb, c = e / nb;
+        sX[c][i] = X[i + (col0 + c) * ldx];
+    }
     __syncthreads();
-    const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (col >= ncols) return;
-    double *xc = X + col * ldx;
+    const int c = threadIdx.x;
     double x[32];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = i < nb ? xc[i] : 0.0;
+    for (int i = 0; i < 32; ++i) x[i] = (i < nb && c < ncl) ? sX[c][i] : 0.0;
     if (LOWER) {  // unit lower, forward: x_i -= T[i,j] x_j, j ascending
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -155,15 +175,21 @@ __global__ void __launch_bounds__(128) tri_cols(const double *__restrict__ T, in
             for (int i = 0; i < j; ++i) x[i] = __dsub_rn(x[i], __dmul_rn(sT[i][j], xj));
         }
     }
+    if (c < ncl)
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-        if (i < nb) xc[i] = x[i];
+        for (int i = 0; i < 32; ++i)
+            if (i < nb) sX[c][i] = x[i];
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb * ncl; e += TC) {
+        const int i = e % nb, cc = e / nb;
+        X[i + (col0 + cc) * ldx] = sX[cc][i];
+    }
 }
 
 template <bool LOWER>
 int tri32(const double *T, int64_t ldt, double *X, int64_t ldx, int nb, int64_t ncols, cudaStream_t s) {
     if (nb <= 0 || ncols <= 0) return 0;
-    tri_cols<LOWER><<<(unsigned)ceil_div(ncols, 128), 128, 0, s>>>(T, ldt, X, ldx, nb, ncols);
+    tri_cols<LOWER><<<(unsigned)ceil_div(ncols, TC), TC, 0, s>>>(T, ldt, X, ldx, nb, ncols);
     LM_LAUNCHED(1);
     return 0;
 }
@@ -204,26 +230,28 @@ __global__ void __launch_bounds__(1024) laswp_plan(const int64_t *__restrict__ p
     if (threadIdx.x == 0) list[0] = count;
 }
 
-// one CTA per column; columns [a0, a1) then [b0, b1)
+// one CTA per column; columns [a0, a1) then [b0, ...)
 __global__ void __launch_bounds__(256) laswp_apply(double *A, int64_t lda, const int32_t *__restrict__ list, int64_t a0,
                                                    int64_t a1, int64_t b0) {
     __shared__ double v[512];
+    const int cnt = list[0];
+    if (cnt == 0) return;
     const int64_t na = a1 - a0;
     const int64_t col = blockIdx.x < na ? a0 + blockIdx.x : b0 + (blockIdx.x - na);
     double *x = A + col * lda;
-    const int cnt = list[0];
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) v[q] = x[list[2 + 2 * q]];
     __syncthreads();
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) x[list[1 + 2 * q]] = v[q];
 }
 
 // ============================================================================
-// the panel: one cluster of CS CTAs holds rows [j0, n) x columns [j0, j0+nb)
+// the panel: one cluster of cs CTAs, rows [j0, n) x columns [j0, j0+nb)
 // ============================================================================
 
-constexpr int PNB = 32;      // panel width
-constexpr int PT = 512;      // threads per CTA
-constexpr int MB = 2 + PNB;  // mailbox slot: value, row, row values
+constexpr int PNB = 32;          // panel width
+constexpr int PT = 512;          // threads per CTA
+constexpr int PW = PT / 32;      // warps per CTA
+constexpr int MB = 2 + PNB;      // mailbox slot: value, row, row values
 
 struct ClusterPanelArgs {
     double *A;
@@ -233,110 +261,107 @@ struct ClusterPanelArgs {
     int32_t *info;
 };
 
-__device__ __forceinline__ bool pbetter(double va, int64_t ia, double vb, int64_t ib) {
+struct PanelSmem {
+    double box[2][MB];         // this CTA's candidate (double-buffered by column parity)
+    double boxk[2][PNB];       // row k, if owned
+    double cand[PW][PNB];      // each warp's candidate row
+    double sU[PNB];            // pivot row
+    double rowk_in[PNB];       // old row k, for the owner of row p
+    double wv[PW];
+    int wi[PW];
+    int s_p;
+};
+
+__device__ __forceinline__ bool pbetter(double va, int ia, double vb, int ib) {
     if (ia < 0) return false;
     if (ib < 0) return true;
     return va > vb || (va == vb && ia < ib);
 }
 
-__global__ void __launch_bounds__(PT) lu_panel_cluster(ClusterPanelArgs a) {
-    extern __shared__ double smp[];
+// Rows are thread-owned, R rows per thread (local rows tid and tid + PT);
+// all register indices are static (the column loop is unrolled).
+template <int R>
+__global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
+    __shared__ PanelSmem sm;
     cg::cluster_group cl = cg::this_cluster();
     const int cs = (int)cl.num_blocks(), me = (int)cl.block_rank();
-    const int ld = PNB + 1;
-    double *sP = smp;                     // [rp][PNB+1]
-    double *box = sP + (int64_t)a.rp * ld;  // [2][MB] candidate mailboxes
-    double *boxk = box + 2 * MB;          // [2][PNB] row-k mailboxes
-    double *sU = boxk + 2 * PNB;          // [PNB] pivot row
-    __shared__ double wv[PT / 32];
-    __shared__ int64_t wi[PT / 32];
-    __shared__ int64_t s_p;
-    __shared__ int s_w;
-
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int nb = a.nb;
-    const int64_t rbeg = a.j0 + (int64_t)me * a.rp;
-    int64_t rend = rbeg + a.rp;
-    if (rend > a.n) rend = a.n;
-    const int nrow = rend > rbeg ? (int)(rend - rbeg) : 0;
-
-    for (int e = tid; e < nrow * nb; e += PT) {
-        const int r = e % nrow, j = e / nrow;
-        sP[r * ld + j] = a.A[(rbeg + r) + (a.j0 + j) * a.lda];
+    // global rows are counted relative to j0 (fits int: n < 2^31)
+    const int rbeg = me * a.rp;
+    const int h = (int)(a.n - a.j0);
+    int rend = rbeg + a.rp;
+    if (rend > h) rend = h;
+    double r[R][PNB];
+    int myrow[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        myrow[q] = rbeg + tid + q * PT;
+        const bool own = myrow[q] < rend;
+#pragma unroll
+        for (int j = 0; j < PNB; ++j)
+            r[q][j] = (own && j < nb) ? a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] : 0.0;
+        if (!own) myrow[q] = -1;
     }
-    __syncthreads();
 
-    for (int kk = 0; kk < nb; ++kk) {
-        const int64_t k = a.j0 + kk;
+#pragma unroll
+    for (int kk = 0; kk < PNB; ++kk) {
+        if (kk >= nb) break;
         const int par = kk & 1;
-        // 1. local candidate (first maximum of |A[i,k]| over owned rows i >= k)
+        // 1. thread / warp candidates: first maximum of |A[i,k]| over rows i >= k
         double bv = -1.0;
-        int64_t bi = -1;
-        for (int r = tid; r < nrow; r += PT) {
-            const int64_t row = rbeg + r;
-            if (row < k) continue;
-            double v = fabs(sP[r * ld + kk]);
+        int bi = -1, bq = 0;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            if (myrow[q] < kk) continue;  // includes the unused rows (-1)
+            double v = fabs(r[q][kk]);
             if (v != v) {
-                if (row != k) continue;
+                if (myrow[q] != kk) continue;
                 v = __longlong_as_double(0x7ff0000000000000LL);
             }
-            if (pbetter(v, row, bv, bi)) {
+            if (pbetter(v, myrow[q], bv, bi)) {
                 bv = v;
-                bi = row;
+                bi = myrow[q];
+                bq = q;
             }
         }
+        double wvv = bv;
+        int wii = bi;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (pbetter(ov, oi, bv, bi)) {
-                bv = ov;
-                bi = oi;
+            const double ov = __shfl_xor_sync(0xffffffffu, wvv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, wii, o);
+            if (pbetter(ov, oi, wvv, wii)) {
+                wvv = ov;
+                wii = oi;
             }
         }
+        // the warp winner publishes its whole panel row (a full-row swap also
+        // moves the multipliers left of k); the owner of row k publishes row k
+        if (wii >= 0 && wii == bi) {
+#pragma unroll
+            for (int j = 0; j < PNB; ++j) sm.cand[wid][j] = r[bq][j];
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            if (myrow[q] == kk) {
+#pragma unroll
+                for (int j = 0; j < PNB; ++j) sm.boxk[par][j] = r[q][j];
+            }
         if (lane == 0) {
-            wv[wid] = bv;
-            wi[wid] = bi;
+            sm.wv[wid] = wvv;
+            sm.wi[wid] = wii;
         }
-        __syncthreads();  // also: every row update of the previous column is done
+        __syncthreads();
+        // 2. CTA candidate -> cluster mailbox
         if (wid == 0) {
-            double v = lane < PT / 32 ? wv[lane] : -1.0;
-            int64_t i = lane < PT / 32 ? wi[lane] : -1;
+            double v = lane < PW ? sm.wv[lane] : -1.0;
+            int i = lane < PW ? sm.wi[lane] : -1;
+            int w = lane;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
-                if (pbetter(ov, oi, v, i)) {
-                    v = ov;
-                    i = oi;
-                }
-            }
-            // 2. publish: candidate value/row and the candidate's row values
-            double *mb = box + par * MB;
-            if (lane == 0) {
-                mb[0] = v;
-                mb[1] = (double)i;
-            }
-            if (i >= 0 && lane < nb) mb[2 + lane] = sP[(i - rbeg) * ld + lane];
-        } else if (wid == 1 && k >= rbeg && k < rend && lane < nb) {
-            boxk[par * PNB + lane] = sP[(k - rbeg) * ld + lane];
-        }
-        cl.sync();  // release the mailboxes / acquire everyone else's
-        // 3. global winner (identical in every CTA)
-        if (wid == 0) {
-            double v = -1.0;
-            int64_t i = -1;
-            int w = -1;
-            if (lane < cs) {
-                const double *rb = cl.map_shared_rank(box + par * MB, lane);
-                v = rb[0];
-                i = (int64_t)rb[1];
-                w = lane;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int64_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, i, o);
                 const int ow = __shfl_xor_sync(0xffffffffu, w, o);
                 if (pbetter(ov, oi, v, i)) {
                     v = ov;
@@ -344,75 +369,113 @@ __global__ void __launch_bounds__(PT) lu_panel_cluster(ClusterPanelArgs a) {
                     w = ow;
                 }
             }
-            if (lane < nb) sU[lane] = cl.map_shared_rank(box + par * MB, w)[2 + lane];
             if (lane == 0) {
-                s_p = i;
-                s_w = w;
+                sm.box[par][0] = v;
+                sm.box[par][1] = (double)i;
+            }
+            if (i >= 0 && lane < PNB) sm.box[par][2 + lane] = sm.cand[w][lane];
+        }
+        cl.sync();
+        // 3. global winner (same answer in every CTA), pivot row, swap data
+        if (wid == 0) {
+            double v = -1.0;
+            int i = -1, w = 0;
+            if (lane < cs) {
+                const double *rb = cl.map_shared_rank(&sm.box[par][0], lane);
+                v = rb[0];
+                i = (int)rb[1];
+                w = lane;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+                const int ow = __shfl_xor_sync(0xffffffffu, w, o);
+                if (pbetter(ov, oi, v, i)) {
+                    v = ov;
+                    i = oi;
+                    w = ow;
+                }
+            }
+            sm.sU[lane] = cl.map_shared_rank(&sm.box[par][0], w)[2 + lane];
+            if (i != kk && i >= rbeg && i < rend) {
+                // this CTA owns row p: it will take the old row k
+                const int owner = kk / a.rp;
+                sm.rowk_in[lane] = cl.map_shared_rank(&sm.boxk[par][0], owner)[lane];
+            }
+            if (lane == 0) {
+                sm.s_p = i;
+                if (me == 0) {
+                    a.piv[a.j0 + kk] = a.j0 + i;
+                    const double pvv = cl.map_shared_rank(&sm.box[par][0], w)[2 + kk];
+                    if (pvv == 0.0 && *a.info == 0) *a.info = (int32_t)(a.j0 + kk + 1);
+                }
             }
         }
         __syncthreads();
-        const int64_t p = s_p;
-        if (me == 0 && tid == 0) {
-            a.piv[k] = p;
-            if (sU[kk] == 0.0 && *a.info == 0) *a.info = (int32_t)(k + 1);
-        }
-        // 4. swap rows k and p inside the panel slice
-        if (p != k) {
-            if (p >= rbeg && p < rend && tid < nb) {
-                const int owner = (int)((k - a.j0) / a.rp);
-                sP[(p - rbeg) * ld + tid] = cl.map_shared_rank(boxk + par * PNB, owner)[tid];
+        const int p = sm.s_p;
+        // 4. swap (rows k and p of the panel), multipliers, rank-1 update
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            if (myrow[q] < 0) continue;
+            if (p != kk) {
+                if (myrow[q] == kk) {
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) r[q][j] = sm.sU[j];
+                } else if (myrow[q] == p) {
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) r[q][j] = sm.rowk_in[j];
+                }
             }
-            if (k >= rbeg && k < rend && tid < nb) sP[(k - rbeg) * ld + tid] = sU[tid];
-        }
-        __syncthreads();
-        // 5. multipliers and the rank-1 update of the panel rows below k
-        const double pv = sU[kk];
-        for (int r = tid; r < nrow; r += PT) {
-            if (rbeg + r <= k) continue;
-            double *row = sP + r * ld;
-            const double m = __ddiv_rn(row[kk], pv);
-            row[kk] = m;
-            for (int j = kk + 1; j < nb; ++j) row[j] = __dsub_rn(row[j], __dmul_rn(m, sU[j]));
+            if (myrow[q] > kk) {
+                const double m = __ddiv_rn(r[q][kk], sm.sU[kk]);
+                r[q][kk] = m;
+#pragma unroll
+                for (int j = kk + 1; j < PNB; ++j) r[q][j] = __dsub_rn(r[q][j], __dmul_rn(m, sm.sU[j]));
+            }
         }
     }
-    cl.sync();  // nobody may exit while its mailboxes can still be read
-    for (int e = tid; e < nrow * nb; e += PT) {
-        const int r = e % nrow, j = e / nrow;
-        a.A[(rbeg + r) + (a.j0 + j) * a.lda] = sP[r * ld + j];
-    }
+    cl.sync();  // no CTA may exit while its mailboxes can still be read
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+        if (myrow[q] >= 0)
+#pragma unroll
+            for (int j = 0; j < PNB; ++j)
+                if (j < nb) a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] = r[q][j];
 }
 
-// cluster size and rows per CTA for a panel of height h; 0 if it does not fit
-static int panel_cluster_size(int64_t h, int &rp) {
-    static int max_cs = -1;
-    if (max_cs < 0) {
-        max_cs = 8;
-        if (cudaFuncSetAttribute(lu_panel_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
-            max_cs = 16;
+static int max_cluster() {
+    static int mc = -1;
+    if (mc < 0) {
+        mc = 8;
+        if (cudaFuncSetAttribute(lu_panel_cluster<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                cudaSuccess &&
+            cudaFuncSetAttribute(lu_panel_cluster<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
+            mc = 16;
     }
-    for (int cs = 1; cs <= max_cs; cs *= 2) {
-        rp = (int)ceil_div(h, cs);
-        if (rp <= 4 * PT / 2 && sizeof(double) * ((size_t)rp * (PNB + 1) + 2 * MB + 3 * PNB) <= 200 * 1024 &&
-            (rp <= PT || cs == max_cs))
-            return cs;
-    }
-    return 0;
+    return mc;
+}
+
+// smallest cluster whose CTAs hold <= R*PT rows each (R = 1 preferred)
+static bool panel_shape(int64_t h, int &cs, int &rp, int &R) {
+    const int mc = max_cluster();
+    for (R = 1; R <= 2; ++R)
+        for (cs = 1; cs <= mc; cs *= 2) {
+            rp = (int)ceil_div(h, cs);
+            if (rp <= R * PT) return true;
+        }
+    return false;
 }
 
 static int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, int nb, int64_t *piv, int32_t *info,
-                                cudaStream_t s, bool &ok) {
-    const int64_t h = n - j0;
-    int rp = 0;
-    const int cs = panel_cluster_size(h, rp);
-    ok = cs > 0;
-    if (!ok) return 0;
-    const size_t smem = sizeof(double) * ((size_t)rp * (PNB + 1) + 2 * MB + 3 * PNB);
-    LM_CUDA(cudaFuncSetAttribute(lu_panel_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                cudaStream_t s) {
+    int cs = 0, rp = 0, R = 0;
+    LM_REQUIRE(panel_shape(n - j0, cs, rp, R), "lu: panel too tall for one cluster");
     ClusterPanelArgs args{A, lda, n, j0, nb, rp, piv, info};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(PT);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -421,12 +484,10 @@ static int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, i
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, lu_panel_cluster, args);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        ok = false;  // cluster not schedulable: caller falls back
-        return 0;
-    }
+    if (R == 1)
+        LM_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_cluster<1>, args));
+    else
+        LM_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_cluster<2>, args));
     count_launch(1);
     return 0;
 }
@@ -455,8 +516,8 @@ constexpr int ONB = 128;  // outer block
 // Returns 1 (and does nothing) when the cluster panel is not usable for
 // this n, so the caller can take the cooperative-grid path.
 int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
-    int rp = 0;
-    if (panel_cluster_size(n, rp) == 0) return 1;
+    int cs = 0, rp = 0, R = 0;
+    if (n >= (1ll << 31) || !panel_shape(n, cs, rp, R) || sizeof(int32_t) * (size_t)n > 200 * 1024) return 1;
     Scratch list;
     if (int rc = list.alloc(sizeof(int32_t) * (1 + 4 * ONB + 8), s)) return rc;
     int32_t *lp = list.as<int32_t>();
@@ -465,9 +526,7 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
         const int64_t J1 = J0 + NBJ;
         for (int64_t j0 = J0; j0 < J1; j0 += PNB) {
             const int nb = (int)((J1 - j0) < PNB ? (J1 - j0) : PNB);
-            bool ok = false;
-            if (int rc = launch_panel_cluster(A, lda, n, j0, nb, piv, info, s, ok)) return rc;
-            LM_REQUIRE(ok, "lu: thread-block cluster for the panel could not be launched");
+            if (int rc = launch_panel_cluster(A, lda, n, j0, nb, piv, info, s)) return rc;
             // this panel's swaps on the rest of the outer block
             if (int rc = laswp(A, lda, n, piv, j0, nb, J0, j0, j0 + nb, J1, lp, s)) return rc;
             const int64_t rest = J1 - (j0 + nb);
