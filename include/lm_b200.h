@@ -166,6 +166,12 @@ int lm_expr_atb_schur_trace_batched(int dtype, int64_t n, int64_t batch, const v
 int lm_fill_uniform(int dtype, lm_view out, uint64_t seed, int64_t row0, int64_t col0, int64_t global_rows,
                     double lo, double hi, void *stream);
 
+/* ---- diagnostics ---------------------------------------------------------- */
+/* Factor one LU panel with the cluster kernel, recording clock64() per
+ * column and phase (4 per column) into d_clock (tools/panel_probe.py). */
+int lm_debug_lu_panel(lm_view a, int64_t j0, int nb, int64_t *d_piv, int32_t *d_info, long long *d_clock,
+                      void *stream);
+
 #ifdef __cplusplus
 }
 #endif

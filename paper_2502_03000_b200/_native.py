@@ -34,6 +34,7 @@ EXPORTS = (
     "lm_analyze", "lm_lu_factor", "lm_lu_solve", "lm_band_solve", "lm_tri_solve",
     "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
     "lm_lu_solve_batched", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
+    "lm_debug_lu_panel",
 )
 
 
@@ -75,6 +76,7 @@ _SIGS = {
     "lm_analyze_batched": (_i, [_i, _i64, _i64, _p, _p, _p]),
     "lm_expr_atb_schur_trace_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "lm_fill_uniform": (_i, [_i, View, ctypes.c_uint64, _i64, _i64, _i64, _d, _d, _p]),
+    "lm_debug_lu_panel": (_i, [View, _i64, _i, _p, _p, _p, _p]),
 }
 
 _lock = threading.Lock()

@@ -244,253 +244,11 @@ __global__ void __launch_bounds__(256) laswp_apply(double *A, int64_t lda, const
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) x[list[1 + 2 * q]] = v[q];
 }
 
-// ============================================================================
-// the panel: one cluster of cs CTAs, rows [j0, n) x columns [j0, j0+nb)
-// ============================================================================
-
-constexpr int PNB = 32;          // panel width
-constexpr int PT = 512;          // threads per CTA
-constexpr int PW = PT / 32;      // warps per CTA
-constexpr int MB = 2 + PNB;      // mailbox slot: value, row, row values
-
-struct ClusterPanelArgs {
-    double *A;
-    int64_t lda, n, j0;
-    int nb, rp;  // panel width, rows per CTA
-    int64_t *piv;
-    int32_t *info;
-};
-
-struct PanelSmem {
-    double box[2][MB];         // this CTA's candidate (double-buffered by column parity)
-    double boxk[2][PNB];       // row k, if owned
-    double cand[PW][PNB];      // each warp's candidate row
-    double sU[PNB];            // pivot row
-    double rowk_in[PNB];       // old row k, for the owner of row p
-    double wv[PW];
-    int wi[PW];
-    int s_p;
-};
-
-__device__ __forceinline__ bool pbetter(double va, int ia, double vb, int ib) {
-    if (ia < 0) return false;
-    if (ib < 0) return true;
-    return va > vb || (va == vb && ia < ib);
-}
-
-// Rows are thread-owned, R rows per thread (local rows tid and tid + PT);
-// all register indices are static (the column loop is unrolled).
-template <int R>
-__global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
-    __shared__ PanelSmem sm;
-    cg::cluster_group cl = cg::this_cluster();
-    const int cs = (int)cl.num_blocks(), me = (int)cl.block_rank();
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int nb = a.nb;
-    // global rows are counted relative to j0 (fits int: n < 2^31)
-    const int rbeg = me * a.rp;
-    const int h = (int)(a.n - a.j0);
-    int rend = rbeg + a.rp;
-    if (rend > h) rend = h;
-    double r[R][PNB];
-    int myrow[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-        myrow[q] = rbeg + tid + q * PT;
-        const bool own = myrow[q] < rend;
-#pragma unroll
-        for (int j = 0; j < PNB; ++j)
-            r[q][j] = (own && j < nb) ? a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] : 0.0;
-        if (!own) myrow[q] = -1;
-    }
-
-#pragma unroll
-    for (int kk = 0; kk < PNB; ++kk) {
-        if (kk >= nb) break;
-        const int par = kk & 1;
-        // 1. thread / warp candidates: first maximum of |A[i,k]| over rows i >= k
-        double bv = -1.0;
-        int bi = -1, bq = 0;
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            if (myrow[q] < kk) continue;  // includes the unused rows (-1)
-            double v = fabs(r[q][kk]);
-            if (v != v) {
-                if (myrow[q] != kk) continue;
-                v = __longlong_as_double(0x7ff0000000000000LL);
-            }
-            if (pbetter(v, myrow[q], bv, bi)) {
-                bv = v;
-                bi = myrow[q];
-                bq = q;
-            }
-        }
-        double wvv = bv;
-        int wii = bi;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, wvv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, wii, o);
-            if (pbetter(ov, oi, wvv, wii)) {
-                wvv = ov;
-                wii = oi;
-            }
-        }
-        // the warp winner publishes its whole panel row (a full-row swap also
-        // moves the multipliers left of k); the owner of row k publishes row k
-        if (wii >= 0 && wii == bi) {
-#pragma unroll
-            for (int j = 0; j < PNB; ++j) sm.cand[wid][j] = r[bq][j];
-        }
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-            if (myrow[q] == kk) {
-#pragma unroll
-                for (int j = 0; j < PNB; ++j) sm.boxk[par][j] = r[q][j];
-            }
-        if (lane == 0) {
-            sm.wv[wid] = wvv;
-            sm.wi[wid] = wii;
-        }
-        __syncthreads();
-        // 2. CTA candidate -> cluster mailbox
-        if (wid == 0) {
-            double v = lane < PW ? sm.wv[lane] : -1.0;
-            int i = lane < PW ? sm.wi[lane] : -1;
-            int w = lane;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, i, o);
-                const int ow = __shfl_xor_sync(0xffffffffu, w, o);
-                if (pbetter(ov, oi, v, i)) {
-                    v = ov;
-                    i = oi;
-                    w = ow;
-                }
-            }
-            if (lane == 0) {
-                sm.box[par][0] = v;
-                sm.box[par][1] = (double)i;
-            }
-            if (i >= 0 && lane < PNB) sm.box[par][2 + lane] = sm.cand[w][lane];
-        }
-        cl.sync();
-        // 3. global winner (same answer in every CTA), pivot row, swap data
-        if (wid == 0) {
-            double v = -1.0;
-            int i = -1, w = 0;
-            if (lane < cs) {
-                const double *rb = cl.map_shared_rank(&sm.box[par][0], lane);
-                v = rb[0];
-                i = (int)rb[1];
-                w = lane;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, i, o);
-                const int ow = __shfl_xor_sync(0xffffffffu, w, o);
-                if (pbetter(ov, oi, v, i)) {
-                    v = ov;
-                    i = oi;
-                    w = ow;
-                }
-            }
-            sm.sU[lane] = cl.map_shared_rank(&sm.box[par][0], w)[2 + lane];
-            if (i != kk && i >= rbeg && i < rend) {
-                // this CTA owns row p: it will take the old row k
-                const int owner = kk / a.rp;
-                sm.rowk_in[lane] = cl.map_shared_rank(&sm.boxk[par][0], owner)[lane];
-            }
-            if (lane == 0) {
-                sm.s_p = i;
-                if (me == 0) {
-                    a.piv[a.j0 + kk] = a.j0 + i;
-                    const double pvv = cl.map_shared_rank(&sm.box[par][0], w)[2 + kk];
-                    if (pvv == 0.0 && *a.info == 0) *a.info = (int32_t)(a.j0 + kk + 1);
-                }
-            }
-        }
-        __syncthreads();
-        const int p = sm.s_p;
-        // 4. swap (rows k and p of the panel), multipliers, rank-1 update
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            if (myrow[q] < 0) continue;
-            if (p != kk) {
-                if (myrow[q] == kk) {
-#pragma unroll
-                    for (int j = 0; j < PNB; ++j) r[q][j] = sm.sU[j];
-                } else if (myrow[q] == p) {
-#pragma unroll
-                    for (int j = 0; j < PNB; ++j) r[q][j] = sm.rowk_in[j];
-                }
-            }
-            if (myrow[q] > kk) {
-                const double m = __ddiv_rn(r[q][kk], sm.sU[kk]);
-                r[q][kk] = m;
-#pragma unroll
-                for (int j = kk + 1; j < PNB; ++j) r[q][j] = __dsub_rn(r[q][j], __dmul_rn(m, sm.sU[j]));
-            }
-        }
-    }
-    cl.sync();  // no CTA may exit while its mailboxes can still be read
-#pragma unroll
-    for (int q = 0; q < R; ++q)
-        if (myrow[q] >= 0)
-#pragma unroll
-            for (int j = 0; j < PNB; ++j)
-                if (j < nb) a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] = r[q][j];
-}
-
-static int max_cluster() {
-    static int mc = -1;
-    if (mc < 0) {
-        mc = 8;
-        if (cudaFuncSetAttribute(lu_panel_cluster<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                cudaSuccess &&
-            cudaFuncSetAttribute(lu_panel_cluster<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
-            mc = 16;
-    }
-    return mc;
-}
-
-// smallest cluster whose CTAs hold <= R*PT rows each (R = 1 preferred)
-static bool panel_shape(int64_t h, int &cs, int &rp, int &R) {
-    const int mc = max_cluster();
-    for (R = 1; R <= 2; ++R)
-        for (cs = 1; cs <= mc; cs *= 2) {
-            rp = (int)ceil_div(h, cs);
-            if (rp <= R * PT) return true;
-        }
-    return false;
-}
-
-static int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, int nb, int64_t *piv, int32_t *info,
-                                cudaStream_t s) {
-    int cs = 0, rp = 0, R = 0;
-    LM_REQUIRE(panel_shape(n - j0, cs, rp, R), "lu: panel too tall for one cluster");
-    ClusterPanelArgs args{A, lda, n, j0, nb, rp, piv, info};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(PT);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (R == 1)
-        LM_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_cluster<1>, args));
-    else
-        LM_CUDA(cudaLaunchKernelEx(&cfg, lu_panel_cluster<2>, args));
-    count_launch(1);
-    return 0;
-}
+// the 32-column panel (lu_panel.cu)
+constexpr int PNB = 32;
+bool panel_shape(int64_t h, int &cs, int &rp, int &R);
+int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, int nb, int64_t *piv, int32_t *info,
+                         cudaStream_t s, long long *dbg = nullptr);
 
 // rows [k0, k0+cnt) pivots applied to columns [a0, a1) U [b0, b1)
 static int laswp(double *A, int64_t lda, int64_t n, const int64_t *piv, int64_t k0, int cnt, int64_t a0, int64_t a1,
