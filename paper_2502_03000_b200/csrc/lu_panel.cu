@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
         if (dbg_on) a.dbg[kk * 4 + 0] = clock64();
         // 1. this thread's best row, then the warp's
         double bv = 0.0;
-        int bq = -1;
+        int bq = -1, brw = 0;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             if (myrow[q] < kk) continue;  // rows above k and unused rows (-1)
@@ -106,14 +106,17 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
             if (bq < 0 || v > bv) {  // R <= 2 and rows ascend with q: strict >
                 bv = v;
                 bq = q;
+                brw = myrow[q];
             }
         }
         unsigned whi, wlo;
-        const int wrow = warp_first_max(bv, bq >= 0, bq >= 0 ? myrow[bq] : 0, whi, wlo);
-        if (bq >= 0 && myrow[bq] == wrow) {
+        const int wrow = warp_first_max(bv, bq >= 0, brw, whi, wlo);
 #pragma unroll
-            for (int j = 0; j < PNB; ++j) sm.cand[wid][j] = r[bq][j];
-        }
+        for (int q = 0; q < R; ++q)  // static register indices only (no local memory)
+            if (q == bq && myrow[q] == wrow) {
+#pragma unroll
+                for (int j = 0; j < PNB; ++j) sm.cand[wid][j] = r[q][j];
+            }
 #pragma unroll
         for (int q = 0; q < R; ++q)
             if (myrow[q] == kk) {
