@@ -26,7 +26,7 @@ namespace cg = cooperative_groups;
 namespace lm {
 
 constexpr int PNB = 32;      // panel width
-constexpr int PT = 512;      // threads per CTA
+constexpr int PT = 256;      // threads per CTA (8 warps: per-warp overheads are issue-bound)
 constexpr int PW = PT / 32;  // warps per CTA
 constexpr int MAXCS = 16;    // largest cluster
 constexpr int SLOT = 2 + PNB;
@@ -47,6 +47,7 @@ struct PanelSmem {
     double rowk[PNB];              // row k, staged for the push
     unsigned whi[PW], wlo[PW];     // warp candidates: |v| bits (+1 on hi), row
     int wrow[PW];
+    int s_p, s_src;                // the column's pivot row and its inbox slot
 };
 
 // (value, row) "first maximum" over the lanes of a warp.  v >= 0 (|A| or
@@ -161,29 +162,31 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
         }
         cl.sync();
         if (dbg_on) a.dbg[kk * 4 + 2] = clock64();
-        // 3. the global winner, computed by every warp from local shared memory
-        double key = -1.0, rowd = -1.0;
-        if (lane < cs) {
-            key = sm.inbox[par][lane][0];
-            rowd = sm.inbox[par][lane][1];
-        }
-        // larger |value| wins, then the lower row (the reference's strict-> scan)
-        double bkey = key, brow = rowd;
-        int bsrc = lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ok = __shfl_xor_sync(0xffffffffu, bkey, o);
-            const double orow = __shfl_xor_sync(0xffffffffu, brow, o);
-            const int osrc = __shfl_xor_sync(0xffffffffu, bsrc, o);
-            const bool take = (orow >= 0.0) && (brow < 0.0 || ok > bkey || (ok == bkey && orow < brow));
-            if (take) {
-                bkey = ok;
-                brow = orow;
-                bsrc = osrc;
+        // 3. the global winner from the local inbox (warp 0), broadcast in smem
+        if (wid == 0) {
+            double key = -1.0, rowd = -1.0;
+            if (lane < cs) {
+                key = sm.inbox[par][lane][0];
+                rowd = sm.inbox[par][lane][1];
+            }
+            // larger |value| wins, then the lower row (the reference's strict-> scan)
+            const bool ok = rowd >= 0.0;
+            const unsigned long long kb = (unsigned long long)__double_as_longlong(key);
+            const unsigned h0 = ok ? (unsigned)(kb >> 32) + 1u : 0u;
+            const unsigned hi = __reduce_max_sync(0xffffffffu, h0);
+            const unsigned l0 = (ok && h0 == hi) ? (unsigned)kb : 0u;
+            const unsigned lo = __reduce_max_sync(0xffffffffu, l0);
+            const unsigned r0 = (ok && h0 == hi && (unsigned)kb == lo) ? (unsigned)rowd : 0xffffffffu;
+            const unsigned row = __reduce_min_sync(0xffffffffu, r0);
+            const unsigned src = __ballot_sync(0xffffffffu, ok && (unsigned)rowd == row);
+            if (lane == 0) {
+                sm.s_p = (int)row;
+                sm.s_src = __ffs(src) - 1;
             }
         }
-        const int p = (int)brow;
-        const double *U = &sm.inbox[par][bsrc][2];
+        __syncthreads();
+        const int p = sm.s_p;
+        const double *U = &sm.inbox[par][sm.s_src][2];
         if (me == 0 && tid == 0) {
             a.piv[a.j0 + kk] = a.j0 + p;
             if (U[kk] == 0.0 && *a.info == 0) *a.info = (int32_t)(a.j0 + kk + 1);
