@@ -48,6 +48,8 @@ struct PanelSmem {
     unsigned whi[PW], wlo[PW];     // warp candidates: |v| bits (+1 on hi), row
     int wrow[PW];
     int s_p, s_src;                // the column's pivot row and its inbox slot
+    double sU[PNB];                // the pivot row (fetched from its CTA)
+    double rowk_in[PNB];           // old row k, for the CTA owning row p
 };
 
 // (value, row) "first maximum" over the lanes of a warp.  v >= 0 (|A| or
@@ -147,18 +149,16 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
             const double hv =
                 hi == 0 ? -1.0 : __longlong_as_double((long long)(((unsigned long long)(hi - 1u) << 32) | lo));
             const double rowv = hi == 0 ? -1.0 : (double)row;
-            const double val = sm.cand[w][lane];
-            for (int t = 0; t < cs; ++t) {
-                double *dst = cl.map_shared_rank(&sm.inbox[par][me][0], t);
-                dst[2 + lane] = val;
-                if (lane == 0) {
-                    dst[0] = hv;
-                    dst[1] = rowv;
-                }
+            // the row stays local (fetched by everyone after the barrier);
+            // only (value, row) is pushed to every CTA -- 2 remote stores per lane
+            sm.inbox[par][me][2 + lane] = sm.cand[w][lane];
+            if (lane < cs) {
+                double *dst = cl.map_shared_rank(&sm.inbox[par][me][0], lane);
+                dst[0] = hv;
+                dst[1] = rowv;
             }
         } else if (wid == 1 && kk >= rbeg && kk < rend) {
-            const double v = sm.rowk[lane];
-            for (int t = 0; t < cs; ++t) cl.map_shared_rank(&sm.inboxk[par][0], t)[lane] = v;
+            sm.inboxk[par][lane] = sm.rowk[lane];
         }
         cl.sync();
         if (dbg_on) a.dbg[kk * 4 + 2] = clock64();
@@ -178,15 +178,17 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
             const unsigned lo = __reduce_max_sync(0xffffffffu, l0);
             const unsigned r0 = (ok && h0 == hi && (unsigned)kb == lo) ? (unsigned)rowd : 0xffffffffu;
             const unsigned row = __reduce_min_sync(0xffffffffu, r0);
-            const unsigned src = __ballot_sync(0xffffffffu, ok && (unsigned)rowd == row);
-            if (lane == 0) {
-                sm.s_p = (int)row;
-                sm.s_src = __ffs(src) - 1;
-            }
+            const unsigned srcm = __ballot_sync(0xffffffffu, ok && (unsigned)rowd == row);
+            const int src = __ffs(srcm) - 1;
+            // one remote round trip: the pivot row (and old row k if we own p)
+            sm.sU[lane] = cl.map_shared_rank(&sm.inbox[par][src][2], src)[lane];
+            if ((int)row != kk && (int)row >= rbeg && (int)row < rend)
+                sm.rowk_in[lane] = cl.map_shared_rank(&sm.inboxk[par][0], kk / a.rp)[lane];
+            if (lane == 0) sm.s_p = (int)row;
         }
         __syncthreads();
         const int p = sm.s_p;
-        const double *U = &sm.inbox[par][sm.s_src][2];
+        const double *U = sm.sU;
         if (me == 0 && tid == 0) {
             a.piv[a.j0 + kk] = a.j0 + p;
             if (U[kk] == 0.0 && *a.info == 0) *a.info = (int32_t)(a.j0 + kk + 1);
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
                     for (int j = 0; j < PNB; ++j) r[q][j] = U[j];
                 } else if (myrow[q] == p) {
 #pragma unroll
-                    for (int j = 0; j < PNB; ++j) r[q][j] = sm.inboxk[par][j];
+                    for (int j = 0; j < PNB; ++j) r[q][j] = sm.rowk_in[j];
                 }
             }
             if (myrow[q] > kk) {
