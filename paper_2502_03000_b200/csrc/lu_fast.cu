@@ -271,48 +271,111 @@ static int laswp(double *A, int64_t lda, int64_t n, const int64_t *piv, int64_t 
 
 constexpr int ONB = 128;  // outer block
 
+// U12 = L11^{-1} A12 and A22 -= L21 U12 for the columns [c0, c1) to the
+// right of outer block [J0, J1) (32-row triangular blocks, order-preserving)
+static int block_right(double *A, int64_t lda, int64_t n, int64_t J0, int64_t J1, int64_t c0, int64_t c1,
+                       cudaStream_t s) {
+    if (c1 <= c0) return 0;
+    const int64_t nc = c1 - c0;
+    for (int64_t b0 = J0; b0 < J1; b0 += PNB) {
+        const int nbb = (int)((J1 - b0) < PNB ? (J1 - b0) : PNB);
+        if (int rc = tri32<true>(A + b0 + b0 * lda, lda, A + b0 + c0 * lda, lda, nbb, nc, s)) return rc;
+        if (b0 + nbb < J1)
+            if (int rc = exact_update<false, false>(A + (b0 + nbb) + b0 * lda, lda, A + b0 + c0 * lda, lda,
+                                                    A + (b0 + nbb) + c0 * lda, lda, J1 - (b0 + nbb), nc, nbb, s))
+                return rc;
+    }
+    return exact_update<false, false>(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1,
+                                      nc, (int)(J1 - J0), s);
+}
+
+struct LuStreams {
+    cudaStream_t hi = nullptr, lo = nullptr;  // panel chain (high priority), look-ahead remainder
+};
+
+static int lu_streams(LuStreams &st) {
+    static LuStreams cache[64];
+    int dev = 0;
+    LM_CUDA(cudaGetDevice(&dev));
+    LM_REQUIRE(dev >= 0 && dev < 64, "device index");
+    if (!cache[dev].hi) {
+        int least = 0, greatest = 0;
+        LM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        LM_CUDA(cudaStreamCreateWithPriority(&cache[dev].hi, cudaStreamNonBlocking, greatest));
+        LM_CUDA(cudaStreamCreateWithPriority(&cache[dev].lo, cudaStreamNonBlocking, least));
+    }
+    st = cache[dev];
+    return 0;
+}
+
 // Returns 1 (and does nothing) when the cluster panel is not usable for
 // this n, so the caller can take the cooperative-grid path.
+//
+// Look-ahead: the panels of block J+1 (critical path, high-priority
+// stream) run while the trailing update of block J's remainder (columns
+// beyond J+1, low-priority stream) is still in flight; the only join is
+// before block J+1's outer row swaps, which touch those columns.
 int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
     int cs = 0, rp = 0, R = 0;
     if (n >= (1ll << 31) || !panel_shape(n, cs, rp, R) || sizeof(int32_t) * (size_t)n > 200 * 1024) return 1;
     Scratch list;
     if (int rc = list.alloc(sizeof(int32_t) * (1 + 4 * ONB + 8), s)) return rc;
     int32_t *lp = list.as<int32_t>();
+    LuStreams st;
+    if (int rc = lu_streams(st)) return rc;
+    cudaEvent_t ev_fork, ev_swapped, ev_rest, ev_join;
+    LM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_swapped, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    struct EvGuard {
+        cudaEvent_t e[4];
+        ~EvGuard() {
+            for (auto x : e) cudaEventDestroy(x);
+        }
+    } guard{{ev_fork, ev_swapped, ev_rest, ev_join}};
+    LM_CUDA(cudaEventRecord(ev_fork, s));
+    LM_CUDA(cudaStreamWaitEvent(st.hi, ev_fork, 0));
+    LM_CUDA(cudaStreamWaitEvent(st.lo, ev_fork, 0));
+    cudaStream_t m = st.hi;
+    bool rest_pending = false;
     for (int64_t J0 = 0; J0 < n; J0 += ONB) {
         const int NBJ = (int)((n - J0) < ONB ? (n - J0) : ONB);
         const int64_t J1 = J0 + NBJ;
         for (int64_t j0 = J0; j0 < J1; j0 += PNB) {
             const int nb = (int)((J1 - j0) < PNB ? (J1 - j0) : PNB);
-            if (int rc = launch_panel_cluster(A, lda, n, j0, nb, piv, info, s)) return rc;
+            if (int rc = launch_panel_cluster(A, lda, n, j0, nb, piv, info, m)) return rc;
             // this panel's swaps on the rest of the outer block
-            if (int rc = laswp(A, lda, n, piv, j0, nb, J0, j0, j0 + nb, J1, lp, s)) return rc;
+            if (int rc = laswp(A, lda, n, piv, j0, nb, J0, j0, j0 + nb, J1, lp, m)) return rc;
             const int64_t rest = J1 - (j0 + nb);
             if (rest > 0) {
-                if (int rc = tri32<true>(A + j0 + j0 * lda, lda, A + j0 + (j0 + nb) * lda, lda, nb, rest, s)) return rc;
+                if (int rc = tri32<true>(A + j0 + j0 * lda, lda, A + j0 + (j0 + nb) * lda, lda, nb, rest, m)) return rc;
                 if (int rc = exact_update<false, false>(A + (j0 + nb) + j0 * lda, lda, A + j0 + (j0 + nb) * lda, lda,
                                                         A + (j0 + nb) + (j0 + nb) * lda, lda, n - (j0 + nb), rest, nb,
-                                                        s))
+                                                        m))
                     return rc;
             }
         }
-        // the outer block's swaps on everything left and right of it
-        if (int rc = laswp(A, lda, n, piv, J0, NBJ, 0, J0, J1, n, lp, s)) return rc;
+        // join the previous block's look-ahead remainder before the outer
+        // swaps (they permute its columns and the L21 it reads)
+        if (rest_pending) LM_CUDA(cudaStreamWaitEvent(m, ev_rest, 0));
+        rest_pending = false;
+        if (int rc = laswp(A, lda, n, piv, J0, NBJ, 0, J0, J1, n, lp, m)) return rc;
         if (J1 < n) {
-            for (int64_t b0 = J0; b0 < J1; b0 += PNB) {
-                const int nbb = (int)((J1 - b0) < PNB ? (J1 - b0) : PNB);
-                if (int rc = tri32<true>(A + b0 + b0 * lda, lda, A + b0 + J1 * lda, lda, nbb, n - J1, s)) return rc;
-                if (b0 + nbb < J1)
-                    if (int rc = exact_update<false, false>(A + (b0 + nbb) + b0 * lda, lda, A + b0 + J1 * lda, lda,
-                                                            A + (b0 + nbb) + J1 * lda, lda, J1 - (b0 + nbb), n - J1,
-                                                            nbb, s))
-                        return rc;
+            const int64_t J2 = (J1 + ONB) < n ? (J1 + ONB) : n;
+            if (J2 < n) {
+                LM_CUDA(cudaEventRecord(ev_swapped, m));
+                LM_CUDA(cudaStreamWaitEvent(st.lo, ev_swapped, 0));
+                if (int rc = block_right(A, lda, n, J0, J1, J2, n, st.lo)) return rc;
+                LM_CUDA(cudaEventRecord(ev_rest, st.lo));
+                rest_pending = true;
             }
-            if (int rc = exact_update<false, false>(A + J1 + J0 * lda, lda, A + J0 + J1 * lda, lda, A + J1 + J1 * lda,
-                                                    lda, n - J1, n - J1, NBJ, s))
-                return rc;
+            if (int rc = block_right(A, lda, n, J0, J1, J1, J2, m)) return rc;  // the next block first
         }
     }
+    if (rest_pending) LM_CUDA(cudaStreamWaitEvent(m, ev_rest, 0));
+    LM_CUDA(cudaEventRecord(ev_join, m));
+    LM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     return 0;
 }
 
