@@ -346,6 +346,7 @@ int launch_trsm(const double *T, int64_t ldt, double *X, int64_t ldx, int nbj, i
 constexpr int kLuNb = 64;
 
 int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s);
+int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s);
 template <bool DESC, bool SKIP_ZERO>
 int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
                  int64_t N, int K, cudaStream_t s);
@@ -434,8 +435,10 @@ int lu_solve_impl(const double *LU, int64_t n, int64_t lda, const int64_t *piv, 
         LM_CUDA(cudaMemcpyAsync(tmp.as<double>() + c * n, X + c * ldx, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     gather_rows<<<(unsigned)ceil_div(n * m, 256), 256, 0, s>>>(tmp.as<double>(), n, perm.as<int32_t>(), n, m, X, ldx);
     LM_LAUNCHED(1);
-    // 2. forward, unit lower: 32-row block (one thread per rhs column), then
-    //    the rows below (order-preserving update, k ascending)
+    // 2./3. one cooperative wavefront kernel for both sweeps (lu_solve.cu)
+    if (int rc = lu_solve_wavefront(LU, n, lda, X, ldx, m, s); rc != 1) return rc;
+    // otherwise: forward, unit lower: 32-row block (one thread per rhs
+    // column), then the rows below (order-preserving update, k ascending)
     constexpr int SB = 32;
     for (int64_t j0 = 0; j0 < n; j0 += SB) {
         const int nbj = (int)((n - j0) < SB ? (n - j0) : SB);

@@ -1,0 +1,170 @@
+// lu_solve.cu -- forward and back substitution for up to 64 right-hand
+// sides (BASELINE config 4a: 8192 x 64) in the reference's exact order
+// (lazymat/_loops.py:239-259: per column, x_i -= L[i,j] x_j for j
+// ascending; then x_j /= U[j,j], x_i -= U[i,j] x_j for j descending; each
+// product and difference rounded, no FMA).
+//
+// One cooperative launch, one CTA per 64-row block ("wavefront"): block I
+// accumulates the contributions of the blocks J < I in ascending J as soon
+// as each one is final (a release/acquire flag per block), then solves its
+// own 64 x 64 triangle (one thread per right-hand side), publishes its rows
+// and raises its flag.  A grid barrier separates the two sweeps; the back
+// sweep runs in descending block order.  The critical path is one triangle
+// per block instead of ~500 dependent kernel launches.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lm {
+
+constexpr int WB = 64;        // rows per block
+constexpr int WM = 64;        // max right-hand sides
+constexpr int WT = 256;       // threads
+constexpr int WLD = WB + 1;   // smem row stride (doubles)
+
+struct WaveArgs {
+    const double *LU;
+    int64_t lda, n;
+    double *X;
+    int64_t ldx;
+    int m, nblk;
+    int *flags;  // [2][nblk], zeroed
+};
+
+__device__ __forceinline__ void wait_flag(const int *f) {
+    if (threadIdx.x == 0) {
+        int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        } while (v == 0);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void raise_flag(int *f) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+    }
+}
+
+__global__ void __launch_bounds__(WT, 1) lu_solve_wave(WaveArgs a) {
+    extern __shared__ double sw[];
+    double *sL = sw;              // [WB][WLD]: sL[i][j] = T[i0+i, j0+j]
+    double *sX = sw + WB * WLD;   // [WB][WLD]: sX[j][c] = X[j0+j, c]
+    double *sY = sX + WB * WLD;   // [WB][WLD]: this block's rows, sY[i][c]
+    cg::grid_group grid = cg::this_grid();
+    const int I = blockIdx.x, tid = threadIdx.x;
+    const int64_t i0 = (int64_t)I * WB;
+    const int rows = (int)((a.n - i0) < WB ? (a.n - i0) : WB);
+    const int tr = tid % 16, tc = tid / 16;  // rows tr + 16a, columns tc + 16b
+    const int m = a.m;
+
+    for (int sweep = 0; sweep < 2; ++sweep) {
+        const bool fwd = sweep == 0;
+        int *flags = a.flags + sweep * a.nblk;
+        // this block's current rows
+        for (int e = tid; e < WB * m; e += WT) {
+            const int i = e % WB, c = e / WB;
+            sY[i * WLD + c] = i < rows ? a.X[(i0 + i) + (int64_t)c * a.ldx] : 0.0;
+        }
+        double acc[4][4];
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) acc[r][s] = sY[(tr + 16 * r) * WLD + tc + 16 * s];
+        // contributions of the other blocks, in the reference's order
+        const int nJ = fwd ? I : a.nblk - 1 - I;
+        for (int t = 0; t < nJ; ++t) {
+            const int J = fwd ? t : a.nblk - 1 - t;
+            const int64_t j0 = (int64_t)J * WB;
+            const int cols = (int)((a.n - j0) < WB ? (a.n - j0) : WB);
+            wait_flag(flags + J);
+            for (int e = tid; e < WB * WB; e += WT) {
+                const int i = e % WB, j = e / WB;
+                sL[i * WLD + j] = (i < rows && j < cols) ? a.LU[(i0 + i) + (j0 + j) * a.lda] : 0.0;
+            }
+            for (int e = tid; e < WB * m; e += WT) {
+                const int j = e % WB, c = e / WB;
+                sX[j * WLD + c] = j < cols ? a.X[(j0 + j) + (int64_t)c * a.ldx] : 0.0;
+            }
+            __syncthreads();
+            for (int q = 0; q < cols; ++q) {
+                const int j = fwd ? q : cols - 1 - q;
+                double l[4], x[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) l[r] = sL[(tr + 16 * r) * WLD + j];
+#pragma unroll
+                for (int s = 0; s < 4; ++s) x[s] = sX[j * WLD + tc + 16 * s];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) acc[r][s] = __dsub_rn(acc[r][s], __dmul_rn(l[r], x[s]));
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) sY[(tr + 16 * r) * WLD + tc + 16 * s] = acc[r][s];
+        // the diagonal triangle
+        for (int e = tid; e < WB * WB; e += WT) {
+            const int i = e % WB, j = e / WB;
+            sL[i * WLD + j] = (i < rows && j < rows) ? a.LU[(i0 + i) + (i0 + j) * a.lda] : 0.0;
+        }
+        __syncthreads();
+        if (tid < m) {  // one thread per right-hand side: sequential substitution
+            const int c = tid;
+            if (fwd) {
+                for (int j = 0; j < rows; ++j) {
+                    const double xj = sY[j * WLD + c];
+                    for (int i = j + 1; i < rows; ++i)
+                        sY[i * WLD + c] = __dsub_rn(sY[i * WLD + c], __dmul_rn(sL[i * WLD + j], xj));
+                }
+            } else {
+                for (int j = rows - 1; j >= 0; --j) {
+                    const double xj = __ddiv_rn(sY[j * WLD + c], sL[j * WLD + j]);
+                    sY[j * WLD + c] = xj;
+                    for (int i = 0; i < j; ++i)
+                        sY[i * WLD + c] = __dsub_rn(sY[i * WLD + c], __dmul_rn(sL[i * WLD + j], xj));
+                }
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < WB * m; e += WT) {
+            const int i = e % WB, c = e / WB;
+            if (i < rows) a.X[(i0 + i) + (int64_t)c * a.ldx] = sY[i * WLD + c];
+        }
+        raise_flag(flags + I);
+        if (fwd) grid.sync();  // every row final before the back sweep reads any
+    }
+}
+
+// 0 = done; 1 = not applicable (caller uses the launch-per-block path)
+int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s) {
+    if (m < 1 || m > WM || n < 1) return 1;
+    const int nblk = (int)ceil_div(n, WB);
+    const size_t smem = sizeof(double) * 3 * WB * WLD;
+    static bool attr = false;
+    if (!attr) {
+        LM_CUDA(cudaFuncSetAttribute(lu_solve_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    int per_sm = 0;
+    LM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_solve_wave, WT, smem));
+    if ((int64_t)per_sm * num_sms() < nblk) return 1;  // all blocks must be co-resident
+    Scratch flags;
+    if (int rc = flags.alloc(sizeof(int) * 2 * nblk, s)) return rc;
+    LM_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 2 * nblk, s));
+    WaveArgs args{LU, lda, n, X, ldx, (int)m, nblk, flags.as<int>()};
+    void *kargs[] = {&args};
+    LM_CUDA(cudaLaunchCooperativeKernel((const void *)lu_solve_wave, dim3(nblk), dim3(WT), kargs, smem, s));
+    count_launch(1);
+    return 0;
+}
+
+}  // namespace lm
