@@ -117,22 +117,42 @@ __global__ void __launch_bounds__(WT, 1) lu_solve_wave(WaveArgs a) {
             sL[i * WLD + j] = (i < rows && j < rows) ? a.LU[(i0 + i) + (i0 + j) * a.lda] : 0.0;
         }
         __syncthreads();
-        if (tid < m) {  // one thread per right-hand side: sequential substitution
-            const int c = tid;
+        {
+            // 4 lanes per right-hand side (consecutive lanes: one warp holds 8
+            // columns), lane g owns rows g, g+4, ..., g+60 in registers; x_j is
+            // broadcast from its owner with one shuffle per step
+            const int c = tid / 4, g = tid % 4;
+            const int base = (tid & 31) & ~3;  // lane of this column's g = 0
+            double x[WB / 4];
+#pragma unroll
+            for (int r = 0; r < WB / 4; ++r) x[r] = (c < m) ? sY[(4 * r + g) * WLD + c] : 0.0;
             if (fwd) {
-                for (int j = 0; j < rows; ++j) {
-                    const double xj = sY[j * WLD + c];
-                    for (int i = j + 1; i < rows; ++i)
-                        sY[i * WLD + c] = __dsub_rn(sY[i * WLD + c], __dmul_rn(sL[i * WLD + j], xj));
+#pragma unroll
+                for (int j = 0; j < WB; ++j) {
+                    if (j >= rows) break;
+                    const double xj = __shfl_sync(0xffffffffu, x[j / 4], base + (j % 4));
+#pragma unroll
+                    for (int r = 0; r < WB / 4; ++r) {
+                        const int i = 4 * r + g;
+                        if (i > j && i < rows) x[r] = __dsub_rn(x[r], __dmul_rn(sL[i * WLD + j], xj));
+                    }
                 }
             } else {
-                for (int j = rows - 1; j >= 0; --j) {
-                    const double xj = __ddiv_rn(sY[j * WLD + c], sL[j * WLD + j]);
-                    sY[j * WLD + c] = xj;
-                    for (int i = 0; i < j; ++i)
-                        sY[i * WLD + c] = __dsub_rn(sY[i * WLD + c], __dmul_rn(sL[i * WLD + j], xj));
+#pragma unroll
+                for (int j = WB - 1; j >= 0; --j) {
+                    if (j >= rows) continue;
+                    if (g == j % 4) x[j / 4] = __ddiv_rn(x[j / 4], sL[j * WLD + j]);
+                    const double xj = __shfl_sync(0xffffffffu, x[j / 4], base + (j % 4));
+#pragma unroll
+                    for (int r = 0; r < WB / 4; ++r) {
+                        const int i = 4 * r + g;
+                        if (i < j) x[r] = __dsub_rn(x[r], __dmul_rn(sL[i * WLD + j], xj));
+                    }
                 }
             }
+            if (c < m)
+#pragma unroll
+                for (int r = 0; r < WB / 4; ++r) sY[(4 * r + g) * WLD + c] = x[r];
         }
         __syncthreads();
         for (int e = tid; e < WB * m; e += WT) {
