@@ -7,13 +7,13 @@
 // pivots untouched).  Thread t keeps ORIGINAL row t of the matrix in N
 // registers for the whole factorisation; the k and j loops are fully
 // unrolled so every register index is static.  Row swaps never move
-// data: a position map (pos[t], row_at[p]) tracks which original row sits
-// at each position, so the reference's "full-row swap" is two integer
-// stores.  Per column k one barrier: each warp publishes its best
-// candidate (|value| desc, position asc -- the reference's strict-> scan)
-// together with the candidate's row, every thread then picks the global
-// winner from the published candidates and reads the pivot row U[k, k+1:]
-// as shared-memory broadcasts.  Multipliers and updates use __ddiv_rn /
+// data: every thread tracks the current position of its row, so the
+// reference's "full-row swap" is two integer assignments.  Per column k
+// one barrier: each warp finds its best candidate (|value| desc, position
+// asc -- the reference's strict-> scan) with three redux.sync
+// instructions and publishes it with the candidate's row; every thread
+// then picks the global winner and reads the pivot row U[k, k+1:] as
+// shared-memory broadcasts.  Multipliers and updates use __ddiv_rn /
 // __dmul_rn / __dsub_rn in the reference order.
 //
 // Traffic per instance: A read once (N*N*8 B), b read, x written; the LU
@@ -28,15 +28,13 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
                                                      int64_t *__restrict__ piv, int32_t *__restrict__ info) {
     constexpr int W = N / 32 > 0 ? N / 32 : 1;  // warps per system
     constexpr unsigned MASK = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
-    constexpr int O0 = N >= 32 ? 16 : N / 2;
     __shared__ double cand_row[2][W][N];        // published candidate rows (double-buffered by k parity)
-    __shared__ double cand_v[2][W];
+    __shared__ unsigned cand_h[2][W], cand_l[2][W];
     __shared__ int cand_pos[2][W], cand_t[2][W];
-    __shared__ int row_at[N];  // position -> original row (thread)
     __shared__ double xb[N];   // substitution broadcast
     __shared__ int s_fail;
 
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int t = threadIdx.x, w = t >> 5;
     const int64_t b = blockIdx.x;
     const double *Ab = A + b * n * n;
     double r[N];
@@ -48,40 +46,38 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
             r[j] = (t == j) ? 1.0 : 0.0;  // identity padding
     }
     double xv = t < n ? __ldg(X + b * n + t) : 0.0;
-    int pos = t;
-    row_at[t] = t;
+    int pos = t;  // current position of the row this thread owns
     if (t == 0) s_fail = 0;
     __syncthreads();
 
 #pragma unroll
     for (int k = 0; k < N; ++k) {
         const int par = k & 1;
-        // --- candidate key of this thread: rows at positions >= k compete
-        double key = -1.0;
+        // --- first maximum of |r[k]| over positions >= k: (|v| bits desc,
+        // position asc) with three redux.sync instructions per warp
+        unsigned hk = 0u, lk = 0u;
         if (pos >= k) {
             double v = fabs(r[k]);
-            if (v != v) v = (pos == k) ? __longlong_as_double(0x7ff0000000000000LL) : -1.0;
-            key = v;
-        }
-        double bk = key;
-        int bp = key >= 0.0 ? pos : 0x7fffffff;
-        int bt = t;
-#pragma unroll
-        for (int o = O0; o > 0; o >>= 1) {
-            const double ok = __shfl_xor_sync(MASK, bk, o);
-            const int op = __shfl_xor_sync(MASK, bp, o);
-            const int ot = __shfl_xor_sync(MASK, bt, o);
-            if (ok > bk || (ok == bk && op < bp)) {
-                bk = ok;
-                bp = op;
-                bt = ot;
+            bool ok = true;
+            if (v != v) {
+                ok = (pos == k);  // NaN never wins off the diagonal; on it, it keeps p = k
+                v = __longlong_as_double(0x7ff0000000000000LL);
+            }
+            if (ok) {
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+                hk = (unsigned)(bits >> 32) + 1u;
+                lk = (unsigned)bits;
             }
         }
-        // warp winner publishes its key, position and row (columns >= k)
-        if (t == bt) {
-            cand_v[par][w] = bk;
-            cand_pos[par][w] = bp;
-            cand_t[par][w] = bt;
+        const unsigned H = __reduce_max_sync(MASK, hk);
+        const unsigned L = __reduce_max_sync(MASK, hk == H ? lk : 0u);
+        const unsigned P = __reduce_min_sync(MASK, (hk != 0u && hk == H && lk == L) ? (unsigned)pos : 0xffffffffu);
+        // the warp winner publishes its key and its row (columns >= k)
+        if (hk != 0u && (unsigned)pos == P) {
+            cand_h[par][w] = H;
+            cand_l[par][w] = L;
+            cand_pos[par][w] = (int)P;
+            cand_t[par][w] = t;
 #pragma unroll
             for (int j = k; j < N; ++j) cand_row[par][w][j] = r[j];
         }
@@ -90,8 +86,10 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
         int win = 0;
 #pragma unroll
         for (int q = 1; q < W; ++q)
-            if (cand_v[par][q] > cand_v[par][win] ||
-                (cand_v[par][q] == cand_v[par][win] && cand_pos[par][q] < cand_pos[par][win]))
+            if (cand_h[par][q] > cand_h[par][win] ||
+                (cand_h[par][q] == cand_h[par][win] &&
+                 (cand_l[par][q] > cand_l[par][win] ||
+                  (cand_l[par][q] == cand_l[par][win] && cand_pos[par][q] < cand_pos[par][win]))))
                 win = q;
         const int p = cand_pos[par][win];   // pivot position (reference's p)
         const int pt = cand_t[par][win];    // the thread holding it
@@ -101,16 +99,12 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
             if (piv && k < n) piv[b * n + k] = p;
             if (pvv == 0.0 && s_fail == 0 && k < n) s_fail = k + 1;
         }
-        // full-row swap of positions k and p == swap of the position map
-        const int tk = row_at[k];
+        // full-row swap of positions k and p == exchange of two positions
         if (p != k) {
-            if (t == pt) pos = k;
-            if (t == tk) pos = p;
-        }
-        __syncthreads();  // everyone has read row_at[k] before it changes
-        if (p != k && t == 0) {
-            row_at[k] = pt;
-            row_at[p] = tk;
+            if (t == pt)
+                pos = k;
+            else if (pos == k)
+                pos = p;
         }
         // multipliers and the rank-1 update of the rows below the pivot
         if (pos > k) {
