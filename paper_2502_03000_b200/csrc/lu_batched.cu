@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
 #pragma unroll
             for (int j = k; j < N; ++j) cand_row[par][w][j] = r[j];
         }
+        if (W > 1 && H == 0u && (t & 31) == 0) cand_h[par][w] = 0u;  // no rows >= k in this warp
         __syncthreads();
         // global winner among the W published candidates
         int win = 0;
