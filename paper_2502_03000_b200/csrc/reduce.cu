@@ -79,6 +79,52 @@ __global__ void __launch_bounds__(256) diag_scale_cols(Vec<const T> d, const T *
     }
 }
 
+// 32-byte-vector column-chunk kernel: CTA c owns the row chunk (c % gx) of
+// the 4 columns 4 * (c / gx) ..; all 4 loads are issued before the first
+// store.  Many short CTAs beat a persistent one-wave grid here (measured on
+// B200 for 128 MB - 2 GB operands, tools/probes/ds_probe.cu: 6.2-6.8 TB/s
+// vs 5.6-5.9 TB/s).  The left scale d[i..i+VN) is loaded once per thread,
+// the right scale d[j] once per column (a warp broadcast).
+template <class T, bool RIGHT>
+__global__ void __launch_bounds__(256) diag_scale_cols32(Vec<const T> d, const T *__restrict__ b, int64_t ldb,
+                                                         T *__restrict__ out, int64_t ldo, int64_t rows, int64_t cols,
+                                                         int gx) {
+    constexpr int VN = Vec32<T>::N;
+    constexpr int U = 4;
+    const int64_t chunk = blockIdx.x / gx;
+    const int64_t i = ((int64_t)(blockIdx.x - chunk * gx) * blockDim.x + threadIdx.x) * VN;
+    if (i >= rows) return;
+    T dl[VN];
+    if (!RIGHT)
+#pragma unroll
+        for (int l = 0; l < VN; ++l) dl[l] = d[i + l];
+    const int64_t j0 = chunk * U;
+    const T *bp = b + i + j0 * ldb;
+    T *op = out + i + j0 * ldo;
+    if (j0 + U <= cols) {
+        Vec32<T> x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = ld_stream32(bp + u * ldb);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const T dj = RIGHT ? d[j0 + u] : T(0);
+            Vec32<T> r;
+#pragma unroll
+            for (int l = 0; l < VN; ++l) r.v[l] = RIGHT ? rmul(x[u].v[l], dj) : rmul(dl[l], x[u].v[l]);
+            st_stream32(op + u * ldo, r);
+        }
+    } else {
+        for (int u = 0; j0 + u < cols; ++u) {
+            const Vec32<T> x = ld_stream32(bp + u * ldb);
+            const T dj = RIGHT ? d[j0 + u] : T(0);
+            Vec32<T> r;
+#pragma unroll
+            for (int l = 0; l < VN; ++l) r.v[l] = RIGHT ? rmul(x.v[l], dj) : rmul(dl[l], x.v[l]);
+            st_stream32(op + u * ldo, r);
+        }
+    }
+}
+
 template <class T, bool RIGHT>
 __global__ void __launch_bounds__(256) diag_scale_strided(Vec<const T> d, View<const T> b, View<T> out, int64_t n) {
     const int64_t nth = (int64_t)gridDim.x * blockDim.x;
@@ -97,6 +143,17 @@ template <class T> int diag_scale_impl(const lm_vec &dv, const lm_view &bv, int 
     if (cm) {
         constexpr int VN = Vec16<T>::N;
         const int64_t ldb = bv.cols > 1 ? bv.cs : bv.rows, ldo = ov.cols > 1 ? ov.cs : ov.rows;
+        constexpr int VN32 = Vec32<T>::N;
+        if (bv.rows % VN32 == 0 && ldb % VN32 == 0 && ldo % VN32 == 0 && aligned32(bv.ptr) && aligned32(ov.ptr)) {
+            const int gx = (int)ceil_div(bv.rows, 256 * VN32);
+            const int64_t grid = gx * ceil_div(bv.cols, 4);
+            if (grid <= 0x7fffffff) {
+                auto kern = side ? diag_scale_cols32<T, true> : diag_scale_cols32<T, false>;
+                kern<<<(unsigned)grid, 256, 0, s>>>(d, (const T *)bv.ptr, ldb, (T *)ov.ptr, ldo, bv.rows, bv.cols, gx);
+                LM_LAUNCHED(1);
+                return 0;
+            }
+        }
         const bool vec = bv.rows % VN == 0 && ldb % VN == 0 && ldo % VN == 0 &&
                          (reinterpret_cast<uintptr_t>(bv.ptr) & 15) == 0 && (reinterpret_cast<uintptr_t>(ov.ptr) & 15) == 0;
         const int64_t gx = ceil_div(bv.rows, 256 * (vec ? VN : 1));
@@ -192,6 +249,74 @@ __global__ void __launch_bounds__(kRedThreads, 2) trace_tiles(View<const T> A, V
     if (threadIdx.x == 0) partials[blockIdx.x] = acc;
 }
 
+// Register-blocked variant for column-major A, B with 4-aligned leading
+// dimensions: each thread loads a 4x4 block of A (A[I..I+3, K..K+3], four
+// 4-element column vectors) and the matching block of B (B[K..K+3, I..I+3])
+// and pairs them in registers -- no shared-memory transpose.  Lane (a, b) =
+// (lane % 4, lane / 4) takes I = 4a, K = 4b inside its warp's 16 x 32
+// sub-tile, so every vector load instruction of a warp touches whole 128 B
+// lines (A: 8 columns x 128 B, B: 4 columns x 256 B).  Per 16 B of input
+// pairs: half a vector load and one FMA (the SMEM version issued ~4
+// instructions per pair and was issue-bound below the HBM rate).
+template <class T> struct Quad {
+    T v[4];
+};
+__device__ __forceinline__ Quad<double> ld_quad(const double *p) {
+    const Vec32<double> x = ld_stream32(p);
+    return Quad<double>{{x.v[0], x.v[1], x.v[2], x.v[3]}};
+}
+__device__ __forceinline__ Quad<float> ld_quad(const float *p) {
+    const float4 x = ld_stream(reinterpret_cast<const float4 *>(p));
+    return Quad<float>{{x.x, x.y, x.z, x.w}};
+}
+
+template <class T, int MINB>
+__global__ void __launch_bounds__(kRedThreads, MINB) trace_quads(View<const T> A, View<const T> B, int64_t ntr,
+                                                             int64_t ntiles, T *__restrict__ partials,
+                                                             unsigned *__restrict__ ticket, T *__restrict__ result) {
+    __shared__ T red[kRedThreads / 32];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int di = 16 * (w & 3) + 4 * (lane & 3);  // I offset in the 64 x 64 tile
+    const int dk = 32 * (w >> 2) + 4 * (lane >> 2);  // K offset
+    const int64_t p = A.rows, q = A.cols;
+    T acc[4] = {T(0), T(0), T(0), T(0)};
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t i0 = (t % ntr) * kTr + di, k0 = (t / ntr) * kTr + dk;
+        if (i0 + 4 <= p && k0 + 4 <= q) {
+            Quad<T> a[4], b[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                a[c] = ld_quad(A.p + i0 + (k0 + c) * A.cs);  // A[i0.., k0+c]
+                b[c] = ld_quad(B.p + k0 + (i0 + c) * B.cs);  // B[k0.., i0+c]
+            }
+#pragma unroll
+            for (int l = 0; l < 4; ++l)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[l] = fma(a[c].v[l], b[l].v[c], acc[l]);  // A[i0+l,k0+c]*B[k0+c,i0+l]
+        } else {
+            for (int l = 0; l < 4; ++l)
+                for (int c = 0; c < 4; ++c)
+                    if (i0 + l < p && k0 + c < q) acc[l] = fma(A(i0 + l, k0 + c), B(k0 + c, i0 + l), acc[l]);
+        }
+    }
+    T v = radd(radd(acc[0], acc[1]), radd(acc[2], acc[3]));
+    v = block_sum<T, kRedThreads>(v, red);
+    // the last CTA to finish sums the partials in index order (fixed tree)
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = v;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    T s = T(0);
+    for (int64_t i = threadIdx.x; i < gridDim.x; i += kRedThreads) s = radd(s, __ldcg(partials + i));
+    s = block_sum<T, kRedThreads>(s, red);
+    if (threadIdx.x == 0) *result = s;
+}
+
 // Sum of `n` partials in index order, fixed tree; writes *out.
 template <class T> __global__ void __launch_bounds__(1024) sum_partials(const T *__restrict__ part, int64_t n, T *out) {
     __shared__ T red[32];
@@ -207,6 +332,26 @@ template <class T> int trace_impl(const lm_view &av, const lm_view &bv, void *d_
     View<const T> B{(const T *)bv.ptr, bv.rows, bv.cols, bv.rs, bv.cs};
     const int64_t ntr = ceil_div(p, kTr), ntc = ceil_div(q, kTr), ntiles = ntr * ntc;
     const bool contig = av.rs == 1 && bv.rs == 1;
+    const bool quads = contig && (av.cols <= 1 || av.cs % 4 == 0) && (bv.cols <= 1 || bv.cs % 4 == 0) &&
+                       (reinterpret_cast<uintptr_t>(av.ptr) & (4 * sizeof(T) - 1)) == 0 &&
+                       (reinterpret_cast<uintptr_t>(bv.ptr) & (4 * sizeof(T) - 1)) == 0;
+    // Large operands (>= 512 MB read): the register-quad kernel with an
+    // 8x oversubscribed grid (6.5-6.9 TB/s at 8192^2-16384^2 f64); below that
+    // the shared-memory kernel's resident wave is faster (6.25 vs 5.9 TB/s at
+    // 4096^2), measured with tools/bw_probe.py.
+    if (quads && ntiles > 0 && 2.0 * p * q * sizeof(T) >= 512.0 * (1 << 20)) {
+        static int res = 0;
+        if (!res) res = resident_grid(trace_quads<T, 2>, kRedThreads);
+        int64_t blocks = (int64_t)res * 8;
+        if (blocks > ntiles) blocks = ntiles;
+        Scratch part;
+        if (int rc = part.alloc(sizeof(T) * blocks + 16, s)) return rc;
+        unsigned *ticket = reinterpret_cast<unsigned *>(part.as<char>() + sizeof(T) * blocks);
+        LM_CUDA(cudaMemsetAsync(ticket, 0, sizeof(unsigned), s));
+        trace_quads<T, 2><<<(unsigned)blocks, kRedThreads, 0, s>>>(A, B, ntr, ntiles, part.as<T>(), ticket, (T *)d_result);
+        LM_LAUNCHED(1);
+        return 0;
+    }
     auto kern = contig ? trace_tiles<T, true> : trace_tiles<T, false>;
     static int grid_cache[2] = {0, 0};
     int &g = grid_cache[contig ? 1 : 0];

@@ -132,6 +132,36 @@ def test_trace_and_diag_of_product(pq, bt):
     assert normwise(host(d), dref) <= 1e-12
 
 
+@pytest.mark.parametrize("pq", [(6000, 5600), (5601, 6004)])
+def test_trace_large_operands(pq):
+    """>= 512 MB of operands takes the register-quad kernel (4-aligned
+    leading dimensions) or, for odd ones, the shared-memory kernel."""
+    p, q = pq
+    rng = np.random.default_rng(p + q)
+    a = np.asfortranarray(rng.uniform(-1, 1, (p, q)))
+    b = np.asfortranarray(rng.uniform(-1, 1, (q, p)))
+    tref = O.trace_of_product(a, b)
+    scale = float(np.sum(np.abs(a) * np.abs(b.T)))
+    t = K.trace_of_product(dev(a), dev(b))
+    assert abs(t - tref) <= 1e-13 * scale
+    assert t == K.trace_of_product(dev(a), dev(b))
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (1028, 6), (4, 4), (8, 3001)])
+@pytest.mark.parametrize("side", ["left", "right"])
+def test_diag_scale_vector_path_bitwise(shape, side):
+    """Row counts divisible by 4 with 32 B-aligned operands take the 32 B
+    vector kernel, including a partial last column chunk."""
+    rng = np.random.default_rng(shape[0] + shape[1])
+    b = np.asfortranarray(rng.uniform(-1, 1, shape))
+    d = rng.uniform(-1, 1, shape[0] if side == "left" else shape[1])
+    ref = np.zeros(shape, order="F")
+    O.diag_scale(d, b, side, ref)
+    out = fortran_empty(*shape, device=DEV)
+    K.diag_scale(torch.from_numpy(d).to(DEV), dev(b), side, out)
+    assert bits_equal(host(out), ref)
+
+
 def test_trace_is_run_to_run_bitwise_reproducible():
     rng = np.random.default_rng(5)
     a = dev(np.asfortranarray(rng.uniform(-1, 1, (777, 555))))
