@@ -85,6 +85,62 @@ __global__ void __launch_bounds__(kGvThreads) gemv_colmajor(View<const T> M, Vec
         if (r0 + r < p) part[blockIdx.y * p + r0 + r] = acc[r];
 }
 
+// Column-major M with 32 B-aligned columns: CTA (rowblock b, chunk c) owns
+// rows [b*RB, b*RB+RB) x columns [c*KC, c*KC+KC).  A thread holds RPT = 32 B
+// of one column (4 doubles / 8 floats); warp w of the CTA takes columns
+// w, w+8, ... of the chunk, so every warp load is one contiguous 1 KB
+// segment and 8 column loads are in flight per thread.  Warp partials are
+// summed in warp order through shared memory into part[chunk][row];
+// gemv_finish sums the chunks in order.  (A last-CTA-finishes ticket
+// variant was no faster: its __threadfence per CTA cost what the second
+// launch does.)
+constexpr int kGv32Warps = 8;
+constexpr int kGv32KC = 64;
+template <class T>
+__global__ void __launch_bounds__(kGv32Warps * 32, 3) gemv_cm32(const T *__restrict__ M, int64_t ld, int64_t p,
+                                                              int64_t q, Vec<const T> x, T *__restrict__ part) {
+    constexpr int RPT = Vec32<T>::N;
+    constexpr int RB = 32 * RPT;  // rows per CTA
+    constexpr int U = kGv32KC / kGv32Warps;  // columns per warp
+    __shared__ T red[kGv32Warps][RB];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t rb = blockIdx.x, c = blockIdx.y;
+    const int64_t r0 = rb * RB + lane * RPT;
+    const int64_t k0 = c * kGv32KC + w;
+    T acc[RPT];
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) acc[l] = T(0);
+    if (r0 < p) {  // p % RPT == 0: a thread's rows are all valid or all not
+        Vec32<T> v[U];
+        T xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = k0 + u * kGv32Warps;
+            if (k < q) {
+                v[u] = ld_stream32(M + r0 + k * ld);
+                xv[u] = x[k];
+            } else {
+#pragma unroll
+                for (int l = 0; l < RPT; ++l) v[u].v[l] = T(0);
+                xv[u] = T(0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int l = 0; l < RPT; ++l) acc[l] = fma(v[u].v[l], xv[u], acc[l]);
+    }
+#pragma unroll
+    for (int l = 0; l < RPT; ++l) red[w][lane * RPT + l] = acc[l];
+    __syncthreads();
+    for (int r = threadIdx.x; r < RB; r += blockDim.x) {
+        T sum = red[0][r];
+#pragma unroll
+        for (int q2 = 1; q2 < kGv32Warps; ++q2) sum += red[q2][r];
+        if (rb * RB + r < p) part[c * p + rb * RB + r] = sum;
+    }
+}
+
 // Row-contiguous (or general) M: one warp per row, lanes along K.
 template <class T>
 __global__ void __launch_bounds__(kGvThreads) gemv_rowmajor(View<const T> M, Vec<const T> x, int64_t kchunk,
@@ -103,13 +159,27 @@ __global__ void __launch_bounds__(kGvThreads) gemv_rowmajor(View<const T> M, Vec
     if (lane == 0) part[blockIdx.y * p + row] = acc;
 }
 
+// y[i] = sum over chunks c (ascending) of part[c][i]: 32 rows per CTA, warp w
+// sums chunks w, w+8, ... (independent loads in flight), the 8 warp sums
+// are added in warp order -- a fixed tree, reproducible run to run.
 template <class T>
 __global__ void __launch_bounds__(256) gemv_finish(const T *__restrict__ part, int64_t p, int64_t nchunks, Vec<T> y) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= p) return;
-    T acc = part[i];
-    for (int64_t c = 1; c < nchunks; ++c) acc += part[c * p + i];
-    y[i] = acc;
+    __shared__ T red[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    T acc = T(0);
+    if (i < p) {
+#pragma unroll 4
+        for (int64_t c = w; c < nchunks; c += 8) acc += part[c * p + i];
+    }
+    red[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && i < p) {
+        T s = red[0][lane];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) s += red[q][lane];
+        y[i] = s;
+    }
 }
 
 template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_vec &yv, cudaStream_t s) {
@@ -118,6 +188,20 @@ template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_v
     View<const T> M{(const T *)mv.ptr, mv.rows, mv.cols, mv.rs, mv.cs};
     Vec<const T> x{(const T *)xv.ptr, xv.n, xv.stride};
     const int nsm = num_sms();
+    constexpr int RPT32 = Vec32<T>::N;
+    if (q > 0 && mv.rs == 1 && p % RPT32 == 0 && (mv.cols <= 1 || mv.cs % RPT32 == 0) && aligned32(mv.ptr) &&
+        ceil_div(q, kGv32KC) <= 65535) {
+        constexpr int RB = 32 * RPT32;
+        const int64_t rowblocks = ceil_div(p, RB), chunks = ceil_div(q, kGv32KC);
+        const int64_t ld = mv.cols > 1 ? mv.cs : p;
+        Scratch part;
+        if (int rc = part.alloc(sizeof(T) * p * chunks, s)) return rc;
+        gemv_cm32<T><<<dim3((unsigned)rowblocks, (unsigned)chunks), kGv32Warps * 32, 0, s>>>((const T *)mv.ptr, ld, p,
+                                                                                            q, x, part.as<T>());
+        gemv_finish<T><<<(unsigned)ceil_div(p, 32), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
+        LM_LAUNCHED(2);
+        return 0;
+    }
     if (mv.rs == 1 || mv.cs != 1) {
         const bool vec2 = sizeof(T) == 8 && mv.rs == 1 && (mv.cs % 2 == 0) && ((uintptr_t)mv.ptr % 16 == 0);
         const int rpt = vec2 ? 2 : 1;
@@ -141,7 +225,7 @@ template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_v
                                                                                                    part.as<T>());
             LM_LAUNCHED(1);
         }
-        gemv_finish<T><<<(unsigned)ceil_div(p, 256), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
+        gemv_finish<T><<<(unsigned)ceil_div(p, 32), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
         LM_LAUNCHED(1);
     } else {
         const int64_t rowblocks = ceil_div(p, kGvThreads / 32);
@@ -158,7 +242,7 @@ template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_v
                                                                                                part.as<T>());
             LM_LAUNCHED(1);
         }
-        gemv_finish<T><<<(unsigned)ceil_div(p, 256), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
+        gemv_finish<T><<<(unsigned)ceil_div(p, 32), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
         LM_LAUNCHED(1);
     }
     return 0;

@@ -228,6 +228,25 @@ def test_gemv_normwise(pq, trans):
     assert normwise(host(out), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("pq", [(4096, 4096), (1028, 100), (8, 3), (516, 65), (2048, 1), (4, 129)])
+def test_gemv_vector_path(pq):
+    """F-contiguous M with p % 4 == 0: the 32 B column kernel with the
+    last-CTA chunk reduction (partial last chunk, single-row-block cases)."""
+    p, q = pq
+    rng = np.random.default_rng(p * 7 + q)
+    a = np.asfortranarray(rng.uniform(-1, 1, (p, q)))
+    x = rng.uniform(-1, 1, q)
+    ref = np.zeros(p)
+    O.gemv(a, x, ref, False)
+    out = torch.empty(p, dtype=torch.float64, device=DEV)
+    da, dx = dev(a), torch.from_numpy(x).to(DEV)
+    K.gemv(da, dx, out, False)
+    assert normwise(host(out), ref) <= 1e-12
+    again = torch.empty_like(out)
+    K.gemv(da, dx, again, False)
+    assert torch.equal(out, again)
+
+
 @pytest.mark.parametrize("n", [1, 2, 5, 17, 64, 65, 100, 200, 333])
 @pytest.mark.parametrize("kind", ["general", "dominant"])
 def test_lu_factor_bitwise_values_and_pivots(n, kind):
