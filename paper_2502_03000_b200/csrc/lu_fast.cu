@@ -12,18 +12,27 @@
 //   outer blocks of ONB = 128 columns (trailing-update K = 128: the A22
 //   read/write traffic is n^3/(3*128) * 16 B, 23 GB at n = 8192);
 //   inside a block, panels of 32 columns factored by ONE thread-block
-//   CLUSTER (up to 16 CTAs of one GPC): every thread keeps one (or two)
-//   panel rows in registers, each column costs one cluster barrier plus
-//   two DSMEM round trips -- candidates and candidate rows are published
-//   in shared-memory mailboxes before the barrier (measured on the B200:
-//   cluster barrier 0.25 us, + DSMEM round 0.2 us; a grid barrier 1.2 us);
+//   CLUSTER (up to 16 CTAs of one GPC, lu_panel.cu): every thread keeps one
+//   (or two) panel rows in registers; per column the CTA candidates are
+//   pushed into every CTA's inbox with st.async + mbarrier transaction
+//   counts, with a one-column look-ahead;
 //   row swaps of the other columns: one composed permutation per panel
 //   (laswp_plan) applied as a gather (laswp_apply);
 //   U12: 32-row triangular solves (smem-staged columns, one thread per
 //   column) + order-preserving updates;
-//   A22: order-preserving SIMT update, 128 x 128 tiles, 8 x 8 per thread,
-//   next K chunk prefetched into registers.
+//   A22: order-preserving SIMT update, 128 x 128 tiles (8 x 8 per thread),
+//   smaller tiles when the grid would not cover the machine, next K chunk
+//   prefetched into registers.
+//
+// LM_LU_TRACE=1 prints a per-step timeline of both streams (debugging).
 #include <cooperative_groups.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <utility>
+#include <vector>
 
 #include "common.cuh"
 
@@ -35,93 +44,126 @@ namespace lm {
 // order-preserving update  C -= A @ B  (k ascending, or descending if DESC)
 // ============================================================================
 
-constexpr int UT = 128, UK = 32, ULD = UT + 1;
+constexpr int UK = 32;  // K chunk staged per step
 
-template <bool DESC, bool SKIP_ZERO>
-__global__ void __launch_bounds__(256) exact_update128(const double *__restrict__ A, int64_t lda,
-                                                       const double *__restrict__ B, int64_t ldb, double *C,
-                                                       int64_t ldc, int64_t M, int64_t N, int K) {
+// C tile (16*RM) x (16*RN) per CTA of 256 threads (16 x 16), RM x RN
+// accumulators per thread; the next K chunk is prefetched into registers
+// while the current one is consumed from shared memory.  Large updates use
+// 128 x 128 tiles (8 x 8 per thread: 1 LDS per 4 exact MACs); narrow or
+// short ones smaller tiles so the grid still covers the machine (a single
+// 128 x 128 tile of a 128 x 128 x 128 update is ~35 us on one SM).
+template <int RM, int RN, bool DESC, bool SKIP_ZERO>
+__global__ void __launch_bounds__(256) exact_update_t(const double *__restrict__ A, int64_t lda,
+                                                      const double *__restrict__ B, int64_t ldb, double *C,
+                                                      int64_t ldc, int64_t M, int64_t N, int K) {
+    constexpr int TM = 16 * RM, TN = 16 * RN;
+    constexpr int LA = TM + 1, LB = TN + 1;
+    constexpr int FA = TM * UK / 256, FB = TN * UK / 256;  // staged elements per thread
     extern __shared__ double su[];
-    double *sA = su;             // [UK][ULD]: sA[kk][ii] = A[i0+ii, k]
-    double *sB = su + UK * ULD;  // [UK][ULD]: sB[kk][cc] = B[k, c0+cc]
+    double *sA = su;             // [UK][LA]: sA[kk][ii] = A[i0+ii, k]
+    double *sB = su + UK * LA;   // [UK][LB]: sB[kk][cc] = B[k, c0+cc]
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t i0 = (int64_t)blockIdx.x * UT, c0 = (int64_t)blockIdx.y * UT;
+    const int64_t i0 = (int64_t)blockIdx.x * TM, c0 = (int64_t)blockIdx.y * TN;
     const int nch = (K + UK - 1) / UK;
-    // staging registers: 16 elements of the A chunk, 16 of the B chunk
-    double pa[16], pb[16];
+    double pa[FA], pb[FB];
     auto fetch = [&](int q) {
         const int k0 = (DESC ? (nch - 1 - q) : q) * UK;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
+        for (int u = 0; u < FA; ++u) {
             const int e = threadIdx.x + 256 * u;
-            const int ii = e % UT, kk = e / UT;
+            const int ii = e % TM, kk = e / TM;
             const int64_t i = i0 + ii;
             const int k = k0 + kk;
             pa[u] = (i < M && k < K) ? __ldg(A + i + (int64_t)k * lda) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < FB; ++u) {
+            const int e = threadIdx.x + 256 * u;
             const int kb = e % UK, cc = e / UK;
             const int64_t c = c0 + cc;
             pb[u] = (c < N && k0 + kb < K) ? __ldg(B + (k0 + kb) + c * ldb) : 0.0;
         }
     };
     fetch(0);
-    double acc[8][8];
+    double acc[RM][RN];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < RM; ++r)
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
+        for (int s = 0; s < RN; ++s) {
             const int64_t i = i0 + tx + 16 * r, c = c0 + ty + 16 * s;
             acc[r][s] = (i < M && c < N) ? C[i + c * ldc] : 0.0;
         }
     for (int q = 0; q < nch; ++q) {
         const int k0 = (DESC ? (nch - 1 - q) : q) * UK;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
+        for (int u = 0; u < FA; ++u) {
             const int e = threadIdx.x + 256 * u;
-            sA[(e / UT) * ULD + e % UT] = pa[u];
-            sB[(e % UK) * ULD + e / UK] = pb[u];
+            sA[(e / TM) * LA + e % TM] = pa[u];
+        }
+#pragma unroll
+        for (int u = 0; u < FB; ++u) {
+            const int e = threadIdx.x + 256 * u;
+            sB[(e % UK) * LB + e / UK] = pb[u];
         }
         __syncthreads();
         if (q + 1 < nch) fetch(q + 1);
         const int kend = (K - k0) < UK ? (K - k0) : UK;
         for (int t = 0; t < kend; ++t) {
             const int kk = DESC ? (kend - 1 - t) : t;
-            double a[8], b[8];
+            double av[RM], bv[RN];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) a[r] = sA[kk * ULD + tx + 16 * r];
+            for (int r = 0; r < RM; ++r) av[r] = sA[kk * LA + tx + 16 * r];
 #pragma unroll
-            for (int s = 0; s < 8; ++s) b[s] = sB[kk * ULD + ty + 16 * s];
+            for (int s = 0; s < RN; ++s) bv[s] = sB[kk * LB + ty + 16 * s];
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
+            for (int r = 0; r < RM; ++r)
 #pragma unroll
-                for (int s = 0; s < 8; ++s)
-                    if (!SKIP_ZERO || b[s] != 0.0) acc[r][s] = __dsub_rn(acc[r][s], __dmul_rn(a[r], b[s]));
+                for (int s = 0; s < RN; ++s)
+                    if (!SKIP_ZERO || bv[s] != 0.0) acc[r][s] = __dsub_rn(acc[r][s], __dmul_rn(av[r], bv[s]));
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+    for (int r = 0; r < RM; ++r)
 #pragma unroll
-        for (int s = 0; s < 8; ++s) {
+        for (int s = 0; s < RN; ++s) {
             const int64_t i = i0 + tx + 16 * r, c = c0 + ty + 16 * s;
             if (i < M && c < N) C[i + c * ldc] = acc[r][s];
         }
 }
 
+template <int RM, int RN, bool DESC, bool SKIP_ZERO>
+int launch_exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
+                        int64_t N, int K, cudaStream_t s) {
+    constexpr int TM = 16 * RM, TN = 16 * RN;
+    const size_t smem = sizeof(double) * UK * (TM + 1 + TN + 1);
+    static bool attr = false;
+    if (!attr) {
+        LM_CUDA(cudaFuncSetAttribute(exact_update_t<RM, RN, DESC, SKIP_ZERO>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    dim3 grid((unsigned)ceil_div(M, TM), (unsigned)ceil_div(N, TN));
+    exact_update_t<RM, RN, DESC, SKIP_ZERO><<<grid, 256, smem, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
+// Tile choice: the largest tile whose grid still gives every SM work
+// (>= 148 CTAs), else the one with the most CTAs.
 template <bool DESC, bool SKIP_ZERO>
 int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
                  int64_t N, int K, cudaStream_t s) {
     if (M <= 0 || N <= 0 || K <= 0) return 0;
-    const size_t smem = sizeof(double) * 2 * UK * ULD;
-    static bool attr = false;
-    if (!attr) {
-        LM_CUDA(cudaFuncSetAttribute(exact_update128<DESC, SKIP_ZERO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        attr = true;
-    }
-    dim3 grid((unsigned)ceil_div(M, UT), (unsigned)ceil_div(N, UT));
-    exact_update128<DESC, SKIP_ZERO><<<grid, 256, smem, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
-    LM_LAUNCHED(1);
-    return 0;
+    const int64_t nsm = num_sms();
+    auto ctas = [&](int tm, int tn) { return ceil_div(M, tm) * ceil_div(N, tn); };
+    if (ctas(128, 128) >= nsm)
+        return launch_exact_update<8, 8, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    if (N > 32 && ctas(64, 64) >= nsm)
+        return launch_exact_update<4, 4, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    if (ctas(64, 32) >= nsm || M > 2048)
+        return launch_exact_update<4, 2, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    return launch_exact_update<2, 2, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
 }
 
 template int exact_update<false, false>(const double *, int64_t, const double *, int64_t, double *, int64_t,
@@ -315,6 +357,47 @@ static int lu_streams(LuStreams &st) {
 // stream) run while the trailing update of block J's remainder (columns
 // beyond J+1, low-priority stream) is still in flight; the only join is
 // before block J+1's outer row swaps, which touch those columns.
+// Debug timeline (LM_LU_TRACE=1): timing events after every step on both
+// streams, printed to stderr as "stream label start_us end_us".
+struct LuTrace {
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, std::string>> ev[2];
+    cudaEvent_t t0 = nullptr;
+    std::chrono::steady_clock::time_point h0;
+    void begin(cudaStream_t s) {
+        on = getenv("LM_LU_TRACE") != nullptr;
+        if (!on) return;
+        h0 = std::chrono::steady_clock::now();
+        cudaEventCreate(&t0);
+        cudaEventRecord(t0, s);
+    }
+    void mark(int which, cudaStream_t s, const std::string &label) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev[which].push_back({e, label});
+    }
+    void dump() {
+        if (!on) return;
+        const double host_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+        cudaDeviceSynchronize();
+        fprintf(stderr, "LUTRACE host issue %.1f us\n", host_us);
+        for (int w = 0; w < 2; ++w) {
+            float prev = 0.f;
+            for (auto &x : ev[w]) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, t0, x.first);
+                fprintf(stderr, "LUTRACE %s %-28s end %10.1f us  (+%8.1f)\n", w ? "lo" : "hi", x.second.c_str(),
+                        ms * 1e3, (ms - prev) * 1e3);
+                prev = ms;
+                cudaEventDestroy(x.first);
+            }
+        }
+        cudaEventDestroy(t0);
+    }
+};
+
 int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
     int cs = 0, rp = 0, R = 0;
     if (n >= (1ll << 31) || !panel_shape(n, cs, rp, R) || sizeof(int32_t) * (size_t)n > 200 * 1024) return 1;
@@ -339,12 +422,15 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
     LM_CUDA(cudaStreamWaitEvent(st.lo, ev_fork, 0));
     cudaStream_t m = st.hi;
     bool rest_pending = false;
+    LuTrace tr;
+    tr.begin(s);
     for (int64_t J0 = 0; J0 < n; J0 += ONB) {
         const int NBJ = (int)((n - J0) < ONB ? (n - J0) : ONB);
         const int64_t J1 = J0 + NBJ;
         for (int64_t j0 = J0; j0 < J1; j0 += PNB) {
             const int nb = (int)((J1 - j0) < PNB ? (J1 - j0) : PNB);
             if (int rc = launch_panel_cluster(A, lda, n, j0, nb, piv, info, m)) return rc;
+            tr.mark(0, m, "panel " + std::to_string(j0));
             // this panel's swaps on the rest of the outer block
             if (int rc = laswp(A, lda, n, piv, j0, nb, J0, j0, j0 + nb, J1, lp, m)) return rc;
             const int64_t rest = J1 - (j0 + nb);
@@ -354,28 +440,37 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
                                                         A + (j0 + nb) + (j0 + nb) * lda, lda, n - (j0 + nb), rest, nb,
                                                         m))
                     return rc;
+                tr.mark(0, m, "inner upd " + std::to_string(j0));
             }
         }
         // join the previous block's look-ahead remainder before the outer
         // swaps (they permute its columns and the L21 it reads)
+        tr.mark(0, m, "chain done " + std::to_string(J0));
         if (rest_pending) LM_CUDA(cudaStreamWaitEvent(m, ev_rest, 0));
         rest_pending = false;
         if (int rc = laswp(A, lda, n, piv, J0, NBJ, 0, J0, J1, n, lp, m)) return rc;
+        tr.mark(0, m, "outer swaps " + std::to_string(J0));
         if (J1 < n) {
             const int64_t J2 = (J1 + ONB) < n ? (J1 + ONB) : n;
             if (J2 < n) {
                 LM_CUDA(cudaEventRecord(ev_swapped, m));
                 LM_CUDA(cudaStreamWaitEvent(st.lo, ev_swapped, 0));
+                // (one kernel per step: column-chunked remainders free SMs for the
+                // panel cluster sooner but lose more in the update tails --
+                // measured 51 ms at one chunk vs 55-121 ms at 2048-256 columns)
                 if (int rc = block_right(A, lda, n, J0, J1, J2, n, st.lo)) return rc;
+                tr.mark(1, st.lo, "remainder " + std::to_string(J0));
                 LM_CUDA(cudaEventRecord(ev_rest, st.lo));
                 rest_pending = true;
             }
             if (int rc = block_right(A, lda, n, J0, J1, J1, J2, m)) return rc;  // the next block first
+            tr.mark(0, m, "next block " + std::to_string(J0));
         }
     }
     if (rest_pending) LM_CUDA(cudaStreamWaitEvent(m, ev_rest, 0));
     LM_CUDA(cudaEventRecord(ev_join, m));
     LM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    tr.dump();
     return 0;
 }
 

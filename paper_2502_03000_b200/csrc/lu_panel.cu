@@ -4,19 +4,27 @@
 // multipliers by __ddiv_rn, rank-1 update with __dmul_rn/__dsub_rn).
 //
 // One thread-block CLUSTER (up to 16 CTAs of a GPC); thread t of CTA c owns
-// panel row c*rp + t in 32 registers for the whole panel.  Per column:
-//   1. each warp finds its candidate with three redux.sync instructions
-//      (max of the high word of |v|, max of the low word, min row) --
-//      the exact "first maximum" order, no shuffles;
-//   2. one __syncthreads; warp 0 forms the CTA candidate and PUSHES it
-//      (value, row, the 32 row values) into the inbox of every CTA of the
-//      cluster with remote DSMEM stores; the owner of row k pushes row k;
-//   3. one cluster barrier (release/acquire) -- after it every CTA holds
-//      all candidates locally: no remote round trip is on the critical
-//      path (measured on the B200: barrier 0.25 us; a DSMEM round 0.2 us);
-//   4. every warp reduces the cs candidates from local shared memory,
-//      swaps (register copies), computes the multiplier and updates its
-//      row from the winner's row in shared memory (broadcast reads).
+// panel rows c*rp + t (+ PT) in registers for the whole panel.  The kernel
+// is issue-bound (every warp executes every column's code), so the design
+// minimises per-warp instructions per column; rare actions (row swaps, row
+// publication) sit behind warp-uniform branches.  Per column c:
+//   1. each warp's first maximum (three redux.sync; |v| bits, then row) and
+//      its candidate row -> local shared memory; one __syncthreads;
+//   2. every warp forms the CTA candidate redundantly and PUSHES (key, row,
+//      32 values) -- and row c if this CTA owns it -- to two target CTAs'
+//      inboxes with st.async (remote stores that complete transaction bytes
+//      on the receiver's mbarrier; no CTA reads remote shared memory, which
+//      serialises on the owner SM's DSMEM port, and there is no cluster
+//      barrier: a release barrier would also wait for outstanding global
+//      stores -- pivots are kept in shared memory until the end);
+//   3. the previous column's update of columns > c runs while the pushes
+//      land; each CTA then waits on its own inbox mbarrier (expected bytes
+//      posted by one thread; the parity alternates every other column);
+//   4. every warp picks the winner among the cs inbox candidates and copies
+//      the pivot row, applying the previous column's update to its columns
+//      > c (the pusher published before applying it; same __dmul_rn /
+//      __dsub_rn on the same operands -- bit-identical), swaps, computes
+//      the multipliers and updates column c+1 first (look-ahead).
 #include <cooperative_groups.h>
 
 #include "common.cuh"
@@ -26,10 +34,9 @@ namespace cg = cooperative_groups;
 namespace lm {
 
 constexpr int PNB = 32;      // panel width
-constexpr int PT = 256;      // threads per CTA (8 warps: per-warp overheads are issue-bound)
+constexpr int PT = 256;      // threads per CTA
 constexpr int PW = PT / 32;  // warps per CTA
 constexpr int MAXCS = 16;    // largest cluster
-constexpr int SLOT = 2 + PNB;
 
 struct ClusterPanelArgs {
     double *A;
@@ -41,20 +48,54 @@ struct ClusterPanelArgs {
 };
 
 struct PanelSmem {
-    double inbox[2][MAXCS][SLOT];  // every CTA's candidate (parity double-buffered)
-    double inboxk[2][PNB];         // row k, pushed by its owner
-    double cand[PW][PNB];          // each warp's candidate row
-    double rowk[PNB];              // row k, staged for the push
-    unsigned whi[PW], wlo[PW];     // warp candidates: |v| bits (+1 on hi), row
-    int wrow[PW];
-    int s_p, s_src;                // the column's pivot row and its inbox slot
-    double sU[PNB];                // the pivot row (fetched from its CTA)
-    double rowk_in[PNB];           // old row k, for the CTA owning row p
+    double ival[2][MAXCS][PNB];         // inbox: each CTA's candidate row
+    unsigned long long ikey[2][MAXCS];  // inbox: candidate keys ((|v| hi + 1) << 32 | lo), 0 = none
+    long long irow[2][MAXCS];           // inbox: candidate rows
+    double ik[2][PNB];                  // inbox: row c (pushed by its owner)
+    unsigned long long bar[2];          // inbox mbarriers (transaction bytes of st.async pushes)
+    double wv[2][PW][PNB];              // local: warp candidate rows
+    unsigned long long wkey[2][PW];     // local: warp candidate keys
+    int wrw[2][PW];                     // local: warp candidate rows
+    double rk[2][PNB];                  // local: row c staged by its owner
+    double U[PW][PNB];                  // per-warp copy of the current pivot row
+    double K[PW][PNB];                  // per-warp copy of old row c (swap partner)
+    long long piv[PNB];                 // pivots (CTA 0), written out at the end
+    long long dclk[PNB * 8];            // debug clocks (CTA 0, thread 0)
 };
 
+__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned cluster_addr(unsigned local, unsigned rank) {
+    unsigned r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+// remote 8-byte store that completes `bytes` on the receiver's mbarrier
+__device__ __forceinline__ void push_f64(unsigned raddr, double v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void push_b64(unsigned raddr, unsigned long long v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v),
+                 "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    unsigned done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+}
+
 // (value, row) "first maximum" over the lanes of a warp.  v >= 0 (|A| or
-// +inf), valid = row participates.  Returns the winning row or -1, and its
-// value bits in (hi, lo) with hi = high word + 1 (0 = none).
+// +inf), valid = row participates.  Returns the winning row, and its value
+// bits in (hi, lo) with hi = high word + 1 (0 = none).
 __device__ __forceinline__ int warp_first_max(double v, bool valid, int row, unsigned &hi, unsigned &lo) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v);
     const unsigned h = valid ? (unsigned)(b >> 32) + 1u : 0u;
@@ -64,6 +105,99 @@ __device__ __forceinline__ int warp_first_max(double v, bool valid, int row, uns
     const unsigned r = (valid && h == hi && (unsigned)b == lo) ? (unsigned)row : 0xffffffffu;
     const unsigned best = __reduce_min_sync(0xffffffffu, r);
     return hi == 0 ? -1 : (int)best;
+}
+
+// (key, row) first maximum over lanes: larger key, then smaller row.
+__device__ __forceinline__ void key_first_max(unsigned long long key, int row, bool valid, unsigned &P,
+                                              unsigned &who, unsigned &H, unsigned &L) {
+    const unsigned h = valid ? (unsigned)(key >> 32) : 0u, l = valid ? (unsigned)key : 0u;
+    H = __reduce_max_sync(0xffffffffu, h);
+    L = __reduce_max_sync(0xffffffffu, h == H ? l : 0u);
+    const bool top = valid && h == H && l == L && H != 0u;
+    P = __reduce_min_sync(0xffffffffu, top ? (unsigned)row : 0xffffffffu);
+    who = __ballot_sync(0xffffffffu, top && (unsigned)row == P);
+}
+
+// steps 1-3 for column c (all indices static after unrolling): candidates,
+// pushes, arrive.
+template <int R>
+__device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const int (&myrow)[R], const int c,
+                                           PanelSmem &sm, cg::cluster_group &cl, int cs, int me, bool own_c) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int par = c & 1;
+    // this thread's best row (rows ascend with q: strict > keeps the first)
+    double bv = 0.0;
+    int bq = -1, brw = 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        if (myrow[q] < c) continue;  // rows above c and unused rows (-1)
+        double v = fabs(r[q][c]);
+        if (v != v) {
+            if (myrow[q] != c) continue;  // NaN never wins off the diagonal
+            v = __longlong_as_double(0x7ff0000000000000LL);
+        }
+        if (bq < 0 || v > bv) {
+            bv = v;
+            bq = q;
+            brw = myrow[q];
+        }
+    }
+    unsigned whi, wlo;
+    const int wrow = warp_first_max(bv, bq >= 0, brw, whi, wlo);
+    // the warp's winning lane publishes its row (one lane per warp)
+    if (whi != 0 && brw == wrow && bq >= 0) {
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            if (q == bq) {
+#pragma unroll
+                for (int j = 0; j < PNB; ++j) sm.wv[par][wid][j] = r[q][j];
+            }
+    }
+    // the owner of row c stages it (whole row: a swap moves the multipliers too)
+    if (own_c) {
+        bool mine = false;
+#pragma unroll
+        for (int q = 0; q < R; ++q) mine |= myrow[q] == c;
+        if (__any_sync(0xffffffffu, mine) && mine) {
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+                if (myrow[q] == c) {
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) sm.rk[par][j] = r[q][j];
+                }
+        }
+    }
+    if (lane == 0) {
+        sm.wkey[par][wid] = whi == 0 ? 0ull : (((unsigned long long)whi << 32) | wlo);
+        sm.wrw[par][wid] = wrow;
+    }
+    __syncthreads();
+    // the CTA candidate (every warp, redundantly) and the pushes
+    unsigned P, who, H, L;
+    {
+        const bool ok = lane < PW;
+        const unsigned long long k = ok ? sm.wkey[par][lane] : 0ull;
+        const int rw = ok ? sm.wrw[par][lane] : 0;
+        key_first_max(k, rw, ok && k != 0ull, P, who, H, L);
+    }
+    const int sw = who ? __ffs(who) - 1 : 0;
+    const unsigned long long key = ((unsigned long long)H << 32) | L;
+    const double myv = sm.wv[par][sw][lane];
+    const double kvv = own_c ? sm.rk[par][lane] : 0.0;
+    const unsigned a_val = smem_addr(&sm.ival[par][me][lane]), a_key = smem_addr(&sm.ikey[par][me]);
+    const unsigned a_row = smem_addr(&sm.irow[par][me]), a_k = smem_addr(&sm.ik[par][lane]);
+    const unsigned a_bar = smem_addr(&sm.bar[par]);
+#pragma unroll
+    for (int t0 = 0; t0 < MAXCS; t0 += PW) {
+        const unsigned t = t0 + wid;
+        if ((int)t < cs) {
+            const unsigned rb = cluster_addr(a_bar, t);
+            push_f64(cluster_addr(a_val, t), myv, rb);
+            if (lane == 0) push_b64(cluster_addr(a_key, t), key, rb);
+            if (lane == 1) push_b64(cluster_addr(a_row, t), (unsigned long long)P, rb);
+            if (own_c) push_f64(cluster_addr(a_k, t), kvv, rb);
+        }
+    }
 }
 
 template <int R>
@@ -89,133 +223,119 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
         if (!own) myrow[q] = -1;
     }
     const bool dbg_on = a.dbg && me == 0 && tid == 0;
-
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.bar[0])), "r"(1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.bar[1])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cl.sync();  // barriers initialised and every CTA running before the first push
+    // bytes arriving per column: cs candidates (row + key + row index) + row c
+    const unsigned col_bytes = (unsigned)cs * (PNB * 8 + 16) + PNB * 8;
+    panel_push<R>(r, myrow, 0, sm, cl, cs, me, 0 >= rbeg && 0 < rend);
+    double u_prev = 0.0;  // previous pivot row, this lane's column
+    int info_col = -1;    // first zero pivot (CTA 0, thread 0)
 #pragma unroll
     for (int kk = 0; kk < PNB; ++kk) {
         if (kk >= nb) break;
         const int par = kk & 1;
-        if (dbg_on) a.dbg[kk * 4 + 0] = clock64();
-        // 1. this thread's best row, then the warp's
-        double bv = 0.0;
-        int bq = -1, brw = 0;
-#pragma unroll
-        for (int q = 0; q < R; ++q) {
-            if (myrow[q] < kk) continue;  // rows above k and unused rows (-1)
-            double v = fabs(r[q][kk]);
-            if (v != v) {
-                if (myrow[q] != kk) continue;  // NaN never wins off the diagonal
-                v = __longlong_as_double(0x7ff0000000000000LL);
-            }
-            if (bq < 0 || v > bv) {  // R <= 2 and rows ascend with q: strict >
-                bv = v;
-                bq = q;
-                brw = myrow[q];
-            }
+        if (dbg_on) sm.dclk[kk * 8 + 0] = clock64();
+        {
+            const unsigned b = smem_addr(&sm.bar[par]);
+            if (tid == 0) mbar_expect(b, col_bytes);
+            mbar_wait(b, (unsigned)(kk >> 1) & 1u);  // column kk's inbox is complete
         }
-        unsigned whi, wlo;
-        const int wrow = warp_first_max(bv, bq >= 0, brw, whi, wlo);
-#pragma unroll
-        for (int q = 0; q < R; ++q)  // static register indices only (no local memory)
-            if (q == bq && myrow[q] == wrow) {
-#pragma unroll
-                for (int j = 0; j < PNB; ++j) sm.cand[wid][j] = r[q][j];
-            }
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-            if (myrow[q] == kk) {
-#pragma unroll
-                for (int j = 0; j < PNB; ++j) sm.rowk[j] = r[q][j];
-            }
-        if (lane == 0) {
-            sm.whi[wid] = whi;
-            sm.wlo[wid] = wlo;
-            sm.wrow[wid] = wrow;
+        if (dbg_on) sm.dclk[kk * 8 + 1] = clock64();
+        // 4. the winner, this warp's copy of the pivot row (+ the missing
+        //    update of column kk-1 on its columns > kk)
+        unsigned P, who, H, L;
+        {
+            const bool ok = lane < cs;
+            const unsigned long long k = ok ? sm.ikey[par][lane] : 0ull;
+            const int rw = ok ? sm.irow[par][lane] : 0;
+            key_first_max(k, rw, ok && k != 0ull, P, who, H, L);
         }
-        __syncthreads();
-        if (dbg_on) a.dbg[kk * 4 + 1] = clock64();
-        // 2. CTA candidate -> every CTA's inbox; row k -> every inbox
-        if (wid == 0) {
-            const bool ok = lane < PW && sm.whi[lane] != 0;
-            const unsigned h0 = ok ? sm.whi[lane] : 0u;
-            const unsigned hi = __reduce_max_sync(0xffffffffu, h0);
-            const unsigned l0 = (ok && h0 == hi) ? sm.wlo[lane] : 0u;
-            const unsigned lo = __reduce_max_sync(0xffffffffu, l0);
-            const unsigned r0 = (ok && h0 == hi && sm.wlo[lane] == lo) ? (unsigned)sm.wrow[lane] : 0xffffffffu;
-            const unsigned row = __reduce_min_sync(0xffffffffu, r0);
-            // the warp that owns the winning row
-            const unsigned wmask = __ballot_sync(0xffffffffu, ok && (unsigned)sm.wrow[lane] == row);
-            const int w = wmask ? __ffs(wmask) - 1 : 0;
-            // the candidate's |value| itself (bits reassembled), -1 for none
-            const double hv =
-                hi == 0 ? -1.0 : __longlong_as_double((long long)(((unsigned long long)(hi - 1u) << 32) | lo));
-            const double rowv = hi == 0 ? -1.0 : (double)row;
-            // the row stays local (fetched by everyone after the barrier);
-            // only (value, row) is pushed to every CTA -- 2 remote stores per lane
-            sm.inbox[par][me][2 + lane] = sm.cand[w][lane];
-            if (lane < cs) {
-                double *dst = cl.map_shared_rank(&sm.inbox[par][me][0], lane);
-                dst[0] = hv;
-                dst[1] = rowv;
+        const int src = who ? __ffs(who) - 1 : 0;
+        const int p = (int)P;
+        {
+            double u = sm.ival[par][src][lane];
+            if (kk > 0) {
+                const double mu = sm.ival[par][src][kk - 1];
+                if (lane > kk) u = __dsub_rn(u, __dmul_rn(mu, u_prev));
             }
-        } else if (wid == 1 && kk >= rbeg && kk < rend) {
-            sm.inboxk[par][lane] = sm.rowk[lane];
-        }
-        cl.sync();
-        if (dbg_on) a.dbg[kk * 4 + 2] = clock64();
-        // 3. the global winner from the local inbox (warp 0), broadcast in smem
-        if (wid == 0) {
-            double key = -1.0, rowd = -1.0;
-            if (lane < cs) {
-                key = sm.inbox[par][lane][0];
-                rowd = sm.inbox[par][lane][1];
+            sm.U[wid][lane] = u;
+            // old row kk: only the warp holding row p needs it
+            bool mine_p = false;
+#pragma unroll
+            for (int q = 0; q < R; ++q) mine_p |= myrow[q] == p;
+            if (p != kk && __any_sync(0xffffffffu, mine_p)) {
+                double kv = sm.ik[par][lane];
+                if (kk > 0) {
+                    const double mk = sm.ik[par][kk - 1];
+                    if (lane > kk) kv = __dsub_rn(kv, __dmul_rn(mk, u_prev));
+                }
+                sm.K[wid][lane] = kv;
             }
-            // larger |value| wins, then the lower row (the reference's strict-> scan)
-            const bool ok = rowd >= 0.0;
-            const unsigned long long kb = (unsigned long long)__double_as_longlong(key);
-            const unsigned h0 = ok ? (unsigned)(kb >> 32) + 1u : 0u;
-            const unsigned hi = __reduce_max_sync(0xffffffffu, h0);
-            const unsigned l0 = (ok && h0 == hi) ? (unsigned)kb : 0u;
-            const unsigned lo = __reduce_max_sync(0xffffffffu, l0);
-            const unsigned r0 = (ok && h0 == hi && (unsigned)kb == lo) ? (unsigned)rowd : 0xffffffffu;
-            const unsigned row = __reduce_min_sync(0xffffffffu, r0);
-            const unsigned srcm = __ballot_sync(0xffffffffu, ok && (unsigned)rowd == row);
-            const int src = __ffs(srcm) - 1;
-            // one remote round trip: the pivot row (and old row k if we own p)
-            sm.sU[lane] = cl.map_shared_rank(&sm.inbox[par][src][2], src)[lane];
-            if ((int)row != kk && (int)row >= rbeg && (int)row < rend)
-                sm.rowk_in[lane] = cl.map_shared_rank(&sm.inboxk[par][0], kk / a.rp)[lane];
-            if (lane == 0) sm.s_p = (int)row;
+            u_prev = u;
+            __syncwarp();
         }
-        __syncthreads();
-        const int p = sm.s_p;
-        const double *U = sm.sU;
+        const double *U = sm.U[wid];
+        const double ukk = U[kk];
         if (me == 0 && tid == 0) {
-            a.piv[a.j0 + kk] = a.j0 + p;
-            if (U[kk] == 0.0 && *a.info == 0) *a.info = (int32_t)(a.j0 + kk + 1);
+            sm.piv[kk] = p;
+            if (ukk == 0.0 && info_col < 0) info_col = kk;
         }
-        if (dbg_on) a.dbg[kk * 4 + 3] = clock64();
-        // 4. swap rows k and p (register copies), multipliers, rank-1 update
+        if (dbg_on) sm.dclk[kk * 8 + 2] = clock64();
+        // full-row swap of rows kk and p (multipliers of columns < kk included)
+        if (p != kk) {
+            bool hit = false;
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-            if (myrow[q] < 0) continue;
-            if (p != kk) {
-                if (myrow[q] == kk) {
+            for (int q = 0; q < R; ++q) hit |= myrow[q] == kk || myrow[q] == p;
+            if (__any_sync(0xffffffffu, hit) && hit) {
+                const double *Kr = sm.K[wid];
 #pragma unroll
-                    for (int j = 0; j < PNB; ++j) r[q][j] = U[j];
-                } else if (myrow[q] == p) {
+                for (int q = 0; q < R; ++q) {
+                    if (myrow[q] == kk) {
 #pragma unroll
-                    for (int j = 0; j < PNB; ++j) r[q][j] = sm.rowk_in[j];
+                        for (int j = 0; j < PNB; ++j) r[q][j] = U[j];
+                    } else if (myrow[q] == p) {
+#pragma unroll
+                        for (int j = 0; j < PNB; ++j) r[q][j] = Kr[j];
+                    }
                 }
             }
-            if (myrow[q] > kk) {
-                const double m = __ddiv_rn(r[q][kk], U[kk]);
-                r[q][kk] = m;
+        }
+        // multipliers, then column kk+1 only
+        double m[R];
+        bool below[R];
 #pragma unroll
-                for (int j = kk + 1; j < PNB; ++j) r[q][j] = __dsub_rn(r[q][j], __dmul_rn(m, U[j]));
+        for (int q = 0; q < R; ++q) {
+            below[q] = myrow[q] > kk;
+            m[q] = 0.0;
+            if (below[q]) {
+                m[q] = __ddiv_rn(r[q][kk], ukk);
+                r[q][kk] = m[q];
+                if (kk + 1 < PNB) r[q][kk + 1] = __dsub_rn(r[q][kk + 1], __dmul_rn(m[q], U[kk + 1]));
             }
         }
+        if (dbg_on) sm.dclk[kk * 8 + 3] = clock64();
+        const bool more = kk + 1 < nb;
+        if (more) panel_push<R>(r, myrow, kk + 1 < PNB ? kk + 1 : 0, sm, cl, cs, me, kk + 1 >= rbeg && kk + 1 < rend);
+        if (dbg_on) sm.dclk[kk * 8 + 6] = clock64();
+        // the rest of the update while the cluster barrier completes
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            if (below[q])
+#pragma unroll
+                for (int j = kk + 2; j < PNB; ++j) r[q][j] = __dsub_rn(r[q][j], __dmul_rn(m[q], U[j]));
+        if (dbg_on) sm.dclk[kk * 8 + 7] = clock64();
     }
-    cl.sync();  // no CTA may exit while others may still write its inbox
+    cl.sync();  // no CTA may exit while others may still write its shared memory
+    if (me == 0 && tid == 0) {
+        for (int k = 0; k < nb; ++k) a.piv[a.j0 + k] = a.j0 + sm.piv[k];
+        if (info_col >= 0 && *a.info == 0) *a.info = (int32_t)(a.j0 + info_col + 1);
+        if (dbg_on)
+            for (int k = 0; k < 8 * nb; ++k) a.dbg[k] = sm.dclk[k];
+    }
 #pragma unroll
     for (int q = 0; q < R; ++q)
         if (myrow[q] >= 0)
@@ -276,7 +396,7 @@ int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, int nb, 
 
 // Diagnostics: factor ONE panel (rows j0.., columns j0..j0+nb) of the F-order
 // n x n matrix with the cluster kernel, recording clock64() per column and
-// phase (CTA 0, thread 0) into d_clock[4*nb].
+// phase (CTA 0, thread 0) into d_clock[8*nb].
 extern "C" int lm_debug_lu_panel(lm_view a, int64_t j0, int nb, int64_t *d_piv, int32_t *d_info, long long *d_clock,
                                  void *stream) {
     lm::clear_error();
