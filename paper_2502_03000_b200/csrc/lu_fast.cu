@@ -45,6 +45,7 @@ namespace lm {
 // ============================================================================
 
 constexpr int UK = 32;  // K chunk staged per step
+static cudaStream_t g_lo_stream = nullptr;  // experiment: the look-ahead stream
 
 // C tile (16*RM) x (16*RN) per CTA of 256 threads (16 x 16), RM x RN
 // accumulators per thread; the next K chunk is prefetched into registers
@@ -157,6 +158,9 @@ int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, dou
     if (M <= 0 || N <= 0 || K <= 0) return 0;
     const int64_t nsm = num_sms();
     auto ctas = [&](int tm, int tn) { return ceil_div(M, tm) * ceil_div(N, tn); };
+    static int lo_tile = getenv("LM_LU_LO_TILE") ? atoi(getenv("LM_LU_LO_TILE")) : 0;
+    if (lo_tile == 64 && g_lo_stream && s == g_lo_stream && N > 32)
+        return launch_exact_update<4, 4, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (ctas(128, 128) >= nsm)
         return launch_exact_update<8, 8, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (N > 32 && ctas(64, 64) >= nsm)
@@ -421,6 +425,7 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
     LM_CUDA(cudaStreamWaitEvent(st.hi, ev_fork, 0));
     LM_CUDA(cudaStreamWaitEvent(st.lo, ev_fork, 0));
     cudaStream_t m = st.hi;
+    g_lo_stream = st.lo;
     bool rest_pending = false;
     LuTrace tr;
     tr.begin(s);
