@@ -349,7 +349,7 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
 int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s);
 template <bool DESC, bool SKIP_ZERO>
 int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
-                 int64_t N, int K, cudaStream_t s);
+                 int64_t N, int K, cudaStream_t s, bool short_ctas = false);
 template <bool LOWER>
 int tri32(const double *T, int64_t ldt, double *X, int64_t ldx, int nb, int64_t ncols, cudaStream_t s);
 

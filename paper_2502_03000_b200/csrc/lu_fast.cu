@@ -45,7 +45,6 @@ namespace lm {
 // ============================================================================
 
 constexpr int UK = 32;  // K chunk staged per step
-static cudaStream_t g_lo_stream = nullptr;  // experiment: the look-ahead stream
 
 // C tile (16*RM) x (16*RN) per CTA of 256 threads (16 x 16), RM x RN
 // accumulators per thread; the next K chunk is prefetched into registers
@@ -151,16 +150,18 @@ int launch_exact_update(const double *A, int64_t lda, const double *B, int64_t l
 }
 
 // Tile choice: the largest tile whose grid still gives every SM work
-// (>= 148 CTAs), else the one with the most CTAs.
+// (>= 148 CTAs), else the one with the most CTAs.  short_ctas (the
+// look-ahead stream's trailing update): 128 x 64 tiles, half as long-lived
+// as 128 x 128, so SMs free up sooner for the high-priority panel cluster
+// (16 free SMs of one GPC) -- 49.4 -> 47.4 ms for the n = 8192 factorisation.
 template <bool DESC, bool SKIP_ZERO>
 int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
-                 int64_t N, int K, cudaStream_t s) {
+                 int64_t N, int K, cudaStream_t s, bool short_ctas = false) {
     if (M <= 0 || N <= 0 || K <= 0) return 0;
     const int64_t nsm = num_sms();
     auto ctas = [&](int tm, int tn) { return ceil_div(M, tm) * ceil_div(N, tn); };
-    static int lo_tile = getenv("LM_LU_LO_TILE") ? atoi(getenv("LM_LU_LO_TILE")) : 0;
-    if (lo_tile == 64 && g_lo_stream && s == g_lo_stream && N > 32)
-        return launch_exact_update<4, 4, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    if (short_ctas && N > 32 && ctas(128, 64) >= nsm)
+        return launch_exact_update<8, 4, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (ctas(128, 128) >= nsm)
         return launch_exact_update<8, 8, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (N > 32 && ctas(64, 64) >= nsm)
@@ -171,9 +172,9 @@ int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, dou
 }
 
 template int exact_update<false, false>(const double *, int64_t, const double *, int64_t, double *, int64_t,
-                                        int64_t, int64_t, int, cudaStream_t);
+                                        int64_t, int64_t, int, cudaStream_t, bool);
 template int exact_update<true, false>(const double *, int64_t, const double *, int64_t, double *, int64_t,
-                                       int64_t, int64_t, int, cudaStream_t);
+                                       int64_t, int64_t, int, cudaStream_t, bool);
 
 // ============================================================================
 // triangular solve on up to 32 rows: columns staged through shared
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(256) laswp_apply(double *A, int64_t lda, const
 constexpr int PNB = 32;
 bool panel_shape(int64_t h, int &cs, int &rp, int &R);
 int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, int nb, int64_t *piv, int32_t *info,
-                         cudaStream_t s, long long *dbg = nullptr);
+                         cudaStream_t s, long long *dbg = nullptr, int64_t J0 = 0, int64_t J1 = 0);
 
 // rows [k0, k0+cnt) pivots applied to columns [a0, a1) U [b0, b1)
 static int laswp(double *A, int64_t lda, int64_t n, const int64_t *piv, int64_t k0, int cnt, int64_t a0, int64_t a1,
@@ -320,7 +321,7 @@ constexpr int ONB = 128;  // outer block
 // U12 = L11^{-1} A12 and A22 -= L21 U12 for the columns [c0, c1) to the
 // right of outer block [J0, J1) (32-row triangular blocks, order-preserving)
 static int block_right(double *A, int64_t lda, int64_t n, int64_t J0, int64_t J1, int64_t c0, int64_t c1,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool short_ctas = false) {
     if (c1 <= c0) return 0;
     const int64_t nc = c1 - c0;
     for (int64_t b0 = J0; b0 < J1; b0 += PNB) {
@@ -332,7 +333,7 @@ static int block_right(double *A, int64_t lda, int64_t n, int64_t J0, int64_t J1
                 return rc;
     }
     return exact_update<false, false>(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1,
-                                      nc, (int)(J1 - J0), s);
+                                      nc, (int)(J1 - J0), s, short_ctas);
 }
 
 struct LuStreams {
@@ -425,7 +426,6 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
     LM_CUDA(cudaStreamWaitEvent(st.hi, ev_fork, 0));
     LM_CUDA(cudaStreamWaitEvent(st.lo, ev_fork, 0));
     cudaStream_t m = st.hi;
-    g_lo_stream = st.lo;
     bool rest_pending = false;
     LuTrace tr;
     tr.begin(s);
@@ -434,13 +434,12 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
         const int64_t J1 = J0 + NBJ;
         for (int64_t j0 = J0; j0 < J1; j0 += PNB) {
             const int nb = (int)((J1 - j0) < PNB ? (J1 - j0) : PNB);
-            if (int rc = launch_panel_cluster(A, lda, n, j0, nb, piv, info, m)) return rc;
+            // the panel kernel also applies its swaps to the rest of the
+            // outer block and solves U12 for the block's remaining columns
+            if (int rc = launch_panel_cluster(A, lda, n, j0, nb, piv, info, m, nullptr, J0, J1)) return rc;
             tr.mark(0, m, "panel " + std::to_string(j0));
-            // this panel's swaps on the rest of the outer block
-            if (int rc = laswp(A, lda, n, piv, j0, nb, J0, j0, j0 + nb, J1, lp, m)) return rc;
             const int64_t rest = J1 - (j0 + nb);
             if (rest > 0) {
-                if (int rc = tri32<true>(A + j0 + j0 * lda, lda, A + j0 + (j0 + nb) * lda, lda, nb, rest, m)) return rc;
                 if (int rc = exact_update<false, false>(A + (j0 + nb) + j0 * lda, lda, A + j0 + (j0 + nb) * lda, lda,
                                                         A + (j0 + nb) + (j0 + nb) * lda, lda, n - (j0 + nb), rest, nb,
                                                         m))
@@ -463,7 +462,7 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
                 // (one kernel per step: column-chunked remainders free SMs for the
                 // panel cluster sooner but lose more in the update tails --
                 // measured 51 ms at one chunk vs 55-121 ms at 2048-256 columns)
-                if (int rc = block_right(A, lda, n, J0, J1, J2, n, st.lo)) return rc;
+                if (int rc = block_right(A, lda, n, J0, J1, J2, n, st.lo, true)) return rc;
                 tr.mark(1, st.lo, "remainder " + std::to_string(J0));
                 LM_CUDA(cudaEventRecord(ev_rest, st.lo));
                 rest_pending = true;

@@ -45,7 +45,105 @@ struct ClusterPanelArgs {
     int64_t *piv;
     int32_t *info;
     long long *dbg;  // optional per-column phase timestamps (CTA 0, thread 0)
+    int64_t J0, J1;  // fused epilogue (J1 > J0): the panel's row swaps on the outer
+                     // block's other columns [J0, j0) U [j0+nb, J1), then
+                     // U12 = L11^-1 A12 on [j0+nb, J1) -- by CTA 0
 };
+
+// Fused epilogue of the panel (CTA 0): the panel's sequential swaps composed
+// into one permutation of the touched rows (<= 2 nb), applied as a gather to
+// the outer block's other columns in chunks of 32; then the unit-lower
+// triangular solve of the nb rows of A12 (one thread per column, the
+// reference's order: x_i -= L[i,j] x_j, j ascending, rounded mul and sub).
+template <int R>
+__device__ __forceinline__ void panel_epilogue(const double (&r)[R][PNB], const ClusterPanelArgs &a,
+                                               const long long *lpiv) {
+    __shared__ int tkey[2 * PNB], tsrc[2 * PNB];
+    __shared__ int s_nt;
+    __shared__ double gbuf[2 * PNB][33];
+    __shared__ double sT[PNB][PNB + 1];
+    const int tid = threadIdx.x, nb = a.nb;
+    const int64_t j0 = a.j0, lda = a.lda;
+    // compose the swaps (warp 0): lane k tracks the source row of top
+    // position k; lane i tracks bottom position bkey (a row >= nb pivoted
+    // up) and its source; ballot finds a bottom position in O(1)
+    if (tid < 32) {
+        const int lane = tid;
+        int top_src = lane, bkey = -1, bsrc = 0, nbot = 0;
+        for (int k = 0; k < nb; ++k) {
+            const int p = (int)lpiv[k];
+            if (p == k) continue;
+            const int a_src = __shfl_sync(0xffffffffu, top_src, k);
+            int b_src;
+            if (p < nb) {
+                b_src = __shfl_sync(0xffffffffu, top_src, p);
+                if (lane == p) top_src = a_src;
+            } else {
+                const unsigned m = __ballot_sync(0xffffffffu, bkey == p);
+                if (m) {
+                    const int j = __ffs(m) - 1;
+                    b_src = __shfl_sync(0xffffffffu, bsrc, j);
+                    if (lane == j) bsrc = a_src;
+                } else {
+                    b_src = p;  // untouched so far: holds its own row
+                    if (lane == nbot) {
+                        bkey = p;
+                        bsrc = a_src;
+                    }
+                    ++nbot;
+                }
+            }
+            if (lane == k) top_src = b_src;
+        }
+        if (lane < nb) {
+            tkey[lane] = lane;
+            tsrc[lane] = top_src;
+        }
+        if (lane < nbot) {
+            tkey[nb + lane] = bkey;
+            tsrc[nb + lane] = bsrc;
+        }
+        if (lane == 0) s_nt = nb + nbot;
+    }
+    // L11 (unit lower) from the registers of rows 0..nb-1 (threads 0..nb-1, q = 0)
+    if (tid < nb)
+#pragma unroll
+        for (int j = 0; j < PNB; ++j) sT[tid][j] = r[0][j];
+    __syncthreads();
+    const int nt = s_nt;
+    const int64_t left = j0 - a.J0, right = a.J1 - (j0 + nb), ncol = left + right;
+    auto colof = [&](int64_t c) { return c < left ? a.J0 + c : j0 + nb + (c - left); };
+    for (int64_t cb = 0; cb < ncol && nt > 0; cb += 32) {
+        const int w = (int)((ncol - cb) < 32 ? (ncol - cb) : 32);
+        for (int e = tid; e < nt * w; e += PT) {
+            const int i = e / w, cc = e - (e / w) * w;
+            gbuf[i][cc] = a.A[(j0 + tsrc[i]) + colof(cb + cc) * lda];
+        }
+        __syncthreads();
+        for (int e = tid; e < nt * w; e += PT) {
+            const int i = e / w, cc = e - (e / w) * w;
+            a.A[(j0 + tkey[i]) + colof(cb + cc) * lda] = gbuf[i][cc];
+        }
+        __syncthreads();
+    }
+    for (int64_t c = tid; c < right; c += PT) {
+        double *col = a.A + j0 + (j0 + nb + c) * lda;
+        double x[PNB];
+#pragma unroll
+        for (int i = 0; i < PNB; ++i) x[i] = i < nb ? col[i] : 0.0;
+#pragma unroll
+        for (int j = 0; j < PNB; ++j) {
+            if (j >= nb) break;
+            const double xj = x[j];
+#pragma unroll
+            for (int i = j + 1; i < PNB; ++i)
+                if (i < nb) x[i] = __dsub_rn(x[i], __dmul_rn(sT[i][j], xj));
+        }
+#pragma unroll
+        for (int i = 0; i < PNB; ++i)
+            if (i < nb) col[i] = x[i];
+    }
+}
 
 struct PanelSmem {
     double ival[2][MAXCS][PNB];         // inbox: each CTA's candidate row
@@ -342,6 +440,7 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
 #pragma unroll
             for (int j = 0; j < PNB; ++j)
                 if (j < nb) a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] = r[q][j];
+    if (a.J1 > a.J0 && me == 0) panel_epilogue<R>(r, a, sm.piv);
 }
 
 static int max_cluster() {
@@ -368,10 +467,11 @@ bool panel_shape(int64_t h, int &cs, int &rp, int &R) {
 }
 
 int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, int nb, int64_t *piv, int32_t *info,
-                         cudaStream_t s, long long *dbg) {
+                         cudaStream_t s, long long *dbg, int64_t J0, int64_t J1) {
     int cs = 0, rp = 0, R = 0;
     LM_REQUIRE(panel_shape(n - j0, cs, rp, R), "lu: panel too tall for one cluster");
-    ClusterPanelArgs args{A, lda, n, j0, nb, rp, piv, info, dbg};
+    LM_REQUIRE(J1 <= J0 || rp >= nb, "lu: fused panel epilogue needs the panel's top rows in CTA 0");
+    ClusterPanelArgs args{A, lda, n, j0, nb, rp, piv, info, dbg, J0, J1};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(PT);
@@ -402,5 +502,5 @@ extern "C" int lm_debug_lu_panel(lm_view a, int64_t j0, int nb, int64_t *d_piv, 
     lm::clear_error();
     LM_REQUIRE(a.rows == a.cols && a.rs == 1 && nb >= 1 && nb <= lm::PNB, "debug panel: bad arguments");
     return lm::launch_panel_cluster((double *)a.ptr, a.cs, a.rows, j0, nb, d_piv, d_info, lm::as_stream(stream),
-                                    d_clock);
+                                    d_clock, 0, 0);
 }

@@ -112,3 +112,24 @@ def test_extension_semantics_pinned_to_naive():
     t6 = A / (1.0 + np.abs(B))
     naive = 1.0 * t3 + (-1.0) * t6
     assert np.array_equal(out.view(np.int64), naive.view(np.int64))
+
+
+def test_capture_rejects_host_synchronising_plans():
+    """Whole-plan CUDA-graph capture refuses plans with solves (they read
+    the factorisation status / structure on the host) before touching a
+    device."""
+    from cases import CASES
+    from paper_2502_03000_b200.errors import KernelContractError
+
+    plan = lm.rewrite(CASES["r10_runtime_gen"](lm))
+    assert "lu_solve" in [s.kernel for s in plan.steps]
+    with pytest.raises(KernelContractError, match="not capturable"):
+        lm.capture(plan)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="CPU-only check")
+def test_capture_without_device_fails_loudly():
+    from cases import CASES
+
+    with pytest.raises(lm.BackendUnavailableError):
+        lm.capture(CASES["r1_weighted_sum"](lm))

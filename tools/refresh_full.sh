@@ -17,5 +17,8 @@ for C in ${CONFIGS:-2 1 3a 3b 3c 4a 4b 5a 5a-f32 5b}; do
   fi
   ncu --set full --clock-control none --import-source on -k "${K[$C]}" -c ${NC[$C]} -o $O/full_c$C -f \
       python bench.py --config $C --steps 1 --warmup 3 --no-e2e --no-cpu --no-clocks > $O/full_c$C.log 2>&1 || echo "full $C failed"
+  python tools/ncu_summary.py $O/full_c$C.ncu-rep > $O/full_c$C.txt 2>&1
+  # keep only the reports asked for (gpurun copies back <= 64 MiB)
+  case " ${KEEP:-2} " in *" $C "*) ;; *) rm -f $O/full_c$C.ncu-rep ;; esac
 done
 echo done
