@@ -219,8 +219,9 @@ __device__ __forceinline__ void key_first_max(unsigned long long key, int row, b
 // steps 1-3 for column c (all indices static after unrolling): candidates,
 // pushes, arrive.
 template <int R>
-__device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const int (&myrow)[R], const int c,
-                                           PanelSmem &sm, cg::cluster_group &cl, int cs, int me, bool own_c) {
+__device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const double (&cv)[R], const int (&myrow)[R],
+                                           const int c, PanelSmem &sm, cg::cluster_group &cl, int cs, int me,
+                                           bool own_c) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int par = c & 1;
     // this thread's best row (rows ascend with q: strict > keeps the first)
@@ -229,7 +230,7 @@ __device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const int 
 #pragma unroll
     for (int q = 0; q < R; ++q) {
         if (myrow[q] < c) continue;  // rows above c and unused rows (-1)
-        double v = fabs(r[q][c]);
+        double v = fabs(cv[q]);
         if (v != v) {
             if (myrow[q] != c) continue;  // NaN never wins off the diagonal
             v = __longlong_as_double(0x7ff0000000000000LL);
@@ -298,59 +299,45 @@ __device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const int 
     }
 }
 
-template <int R>
-__global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
-    __shared__ PanelSmem sm;
-    cg::cluster_group cl = cg::this_cluster();
-    const int cs = (int)cl.num_blocks(), me = (int)cl.block_rank();
+// Columns [K0, K0 + PKB) of the panel with a run-time column index kk: the
+// body is emitted once per block of 8 columns (a fully unrolled 32-column
+// kernel is ~21k instructions and stalls on instruction fetch: ncu
+// no_instruction 12 of 20 stall cycles per issue).  Register indices stay
+// static: the j loops start at the block's K0 and predicate on j vs kk.
+constexpr int PKB = 8;
+
+struct PanelLoop {
+    int cs, me, rbeg, rend, nb;
+    unsigned col_bytes;
+    bool dbg_on;
+    double u_prev;
+    int info_col;
+};
+
+template <int R, int K0>
+__device__ __forceinline__ void panel_cols(double (&r)[R][PNB], const int (&myrow)[R], PanelSmem &sm,
+                                           cg::cluster_group &cl, PanelLoop &L) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int nb = a.nb;
-    const int rbeg = me * a.rp;  // rows counted from j0
-    const int h = (int)(a.n - a.j0);
-    int rend = rbeg + a.rp;
-    if (rend > h) rend = h;
-    double r[R][PNB];
-    int myrow[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) {
-        myrow[q] = rbeg + tid + q * PT;
-        const bool own = myrow[q] < rend;
-#pragma unroll
-        for (int j = 0; j < PNB; ++j)
-            r[q][j] = (own && j < nb) ? a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] : 0.0;
-        if (!own) myrow[q] = -1;
-    }
-    const bool dbg_on = a.dbg && me == 0 && tid == 0;
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.bar[0])), "r"(1));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.bar[1])), "r"(1));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    cl.sync();  // barriers initialised and every CTA running before the first push
-    // bytes arriving per column: cs candidates (row + key + row index) + row c
-    const unsigned col_bytes = (unsigned)cs * (PNB * 8 + 16) + PNB * 8;
-    panel_push<R>(r, myrow, 0, sm, cl, cs, me, 0 >= rbeg && 0 < rend);
-    double u_prev = 0.0;  // previous pivot row, this lane's column
-    int info_col = -1;    // first zero pivot (CTA 0, thread 0)
-#pragma unroll
-    for (int kk = 0; kk < PNB; ++kk) {
-        if (kk >= nb) break;
+    constexpr int KE = K0 + PKB;
+    const int kend = KE < L.nb ? KE : L.nb;
+#pragma unroll 1
+    for (int kk = K0; kk < kend; ++kk) {
         const int par = kk & 1;
-        if (dbg_on) sm.dclk[kk * 8 + 0] = clock64();
+        if (L.dbg_on) sm.dclk[kk * 8 + 0] = clock64();
         {
             const unsigned b = smem_addr(&sm.bar[par]);
-            if (tid == 0) mbar_expect(b, col_bytes);
+            if (tid == 0) mbar_expect(b, L.col_bytes);
             mbar_wait(b, (unsigned)(kk >> 1) & 1u);  // column kk's inbox is complete
         }
-        if (dbg_on) sm.dclk[kk * 8 + 1] = clock64();
-        // 4. the winner, this warp's copy of the pivot row (+ the missing
-        //    update of column kk-1 on its columns > kk)
-        unsigned P, who, H, L;
+        if (L.dbg_on) sm.dclk[kk * 8 + 1] = clock64();
+        // the winner, this warp's copy of the pivot row (+ the missing update
+        // of column kk-1 on its columns > kk)
+        unsigned P, who, H, Lo;
         {
-            const bool ok = lane < cs;
+            const bool ok = lane < L.cs;
             const unsigned long long k = ok ? sm.ikey[par][lane] : 0ull;
             const int rw = ok ? sm.irow[par][lane] : 0;
-            key_first_max(k, rw, ok && k != 0ull, P, who, H, L);
+            key_first_max(k, rw, ok && k != 0ull, P, who, H, Lo);
         }
         const int src = who ? __ffs(who) - 1 : 0;
         const int p = (int)P;
@@ -358,10 +345,9 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
             double u = sm.ival[par][src][lane];
             if (kk > 0) {
                 const double mu = sm.ival[par][src][kk - 1];
-                if (lane > kk) u = __dsub_rn(u, __dmul_rn(mu, u_prev));
+                if (lane > kk) u = __dsub_rn(u, __dmul_rn(mu, L.u_prev));
             }
             sm.U[wid][lane] = u;
-            // old row kk: only the warp holding row p needs it
             bool mine_p = false;
 #pragma unroll
             for (int q = 0; q < R; ++q) mine_p |= myrow[q] == p;
@@ -369,20 +355,20 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
                 double kv = sm.ik[par][lane];
                 if (kk > 0) {
                     const double mk = sm.ik[par][kk - 1];
-                    if (lane > kk) kv = __dsub_rn(kv, __dmul_rn(mk, u_prev));
+                    if (lane > kk) kv = __dsub_rn(kv, __dmul_rn(mk, L.u_prev));
                 }
                 sm.K[wid][lane] = kv;
             }
-            u_prev = u;
+            L.u_prev = u;
             __syncwarp();
         }
         const double *U = sm.U[wid];
         const double ukk = U[kk];
-        if (me == 0 && tid == 0) {
+        if (L.me == 0 && tid == 0) {
             sm.piv[kk] = p;
-            if (ukk == 0.0 && info_col < 0) info_col = kk;
+            if (ukk == 0.0 && L.info_col < 0) L.info_col = kk;
         }
-        if (dbg_on) sm.dclk[kk * 8 + 2] = clock64();
+        if (L.dbg_on) sm.dclk[kk * 8 + 2] = clock64();
         // full-row swap of rows kk and p (multipliers of columns < kk included)
         if (p != kk) {
             bool hit = false;
@@ -403,35 +389,105 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
             }
         }
         // multipliers, then column kk+1 only
-        double m[R];
+        double m[R], cn[R];
         bool below[R];
+        const double u1 = kk + 1 < PNB ? U[kk + 1] : 0.0;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
             below[q] = myrow[q] > kk;
-            m[q] = 0.0;
-            if (below[q]) {
-                m[q] = __ddiv_rn(r[q][kk], ukk);
-                r[q][kk] = m[q];
-                if (kk + 1 < PNB) r[q][kk + 1] = __dsub_rn(r[q][kk + 1], __dmul_rn(m[q], U[kk + 1]));
-            }
+            double ck = r[q][K0];
+#pragma unroll
+            for (int j = K0 + 1; j < KE && j < PNB; ++j)
+                if (kk == j) ck = r[q][j];
+            m[q] = below[q] ? __ddiv_rn(ck, ukk) : 0.0;
+            double c1 = r[q][K0 + 1 < PNB ? K0 + 1 : PNB - 1];
+#pragma unroll
+            for (int j = K0 + 2; j <= KE && j < PNB; ++j)
+                if (kk + 1 == j) c1 = r[q][j];
+            if (below[q]) c1 = __dsub_rn(c1, __dmul_rn(m[q], u1));
+            cn[q] = c1;
+#pragma unroll
+            for (int j = K0; j < KE && j < PNB; ++j)
+                if (below[q] && j == kk) r[q][j] = m[q];
+#pragma unroll
+            for (int j = K0 + 1; j <= KE && j < PNB; ++j)
+                if (below[q] && j == kk + 1) r[q][j] = c1;
         }
-        if (dbg_on) sm.dclk[kk * 8 + 3] = clock64();
-        const bool more = kk + 1 < nb;
-        if (more) panel_push<R>(r, myrow, kk + 1 < PNB ? kk + 1 : 0, sm, cl, cs, me, kk + 1 >= rbeg && kk + 1 < rend);
-        if (dbg_on) sm.dclk[kk * 8 + 6] = clock64();
-        // the rest of the update while the cluster barrier completes
+        if (L.dbg_on) sm.dclk[kk * 8 + 3] = clock64();
+        if (kk + 1 < L.nb) {
+            const int c = kk + 1;
+            panel_push<R>(r, cn, myrow, c, sm, cl, L.cs, L.me, c >= L.rbeg && c < L.rend);
+        }
+        if (L.dbg_on) sm.dclk[kk * 8 + 6] = clock64();
+        // the rest of the update while the pushes land
 #pragma unroll
         for (int q = 0; q < R; ++q)
-            if (below[q])
+            if (below[q]) {
 #pragma unroll
-                for (int j = kk + 2; j < PNB; ++j) r[q][j] = __dsub_rn(r[q][j], __dmul_rn(m[q], U[j]));
-        if (dbg_on) sm.dclk[kk * 8 + 7] = clock64();
+                for (int j = K0 + 2; j <= KE && j < PNB; ++j)
+                    if (j > kk + 1) r[q][j] = __dsub_rn(r[q][j], __dmul_rn(m[q], U[j]));
+#pragma unroll
+                for (int j = KE + 1; j < PNB; ++j) r[q][j] = __dsub_rn(r[q][j], __dmul_rn(m[q], U[j]));
+            }
+        if (L.dbg_on) sm.dclk[kk * 8 + 7] = clock64();
     }
+}
+
+template <int R>
+__global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
+    __shared__ PanelSmem sm;
+    cg::cluster_group cl = cg::this_cluster();
+    const int cs = (int)cl.num_blocks(), me = (int)cl.block_rank();
+    const int tid = threadIdx.x;
+    const int nb = a.nb;
+    const int rbeg = me * a.rp;  // rows counted from j0
+    const int h = (int)(a.n - a.j0);
+    int rend = rbeg + a.rp;
+    if (rend > h) rend = h;
+    double r[R][PNB];
+    int myrow[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        myrow[q] = rbeg + tid + q * PT;
+        const bool own = myrow[q] < rend;
+#pragma unroll
+        for (int j = 0; j < PNB; ++j)
+            r[q][j] = (own && j < nb) ? a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] : 0.0;
+        if (!own) myrow[q] = -1;
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.bar[0])), "r"(1));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&sm.bar[1])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cl.sync();  // barriers initialised and every CTA running before the first push
+    PanelLoop L;
+    L.cs = cs;
+    L.me = me;
+    L.rbeg = rbeg;
+    L.rend = rend;
+    L.nb = nb;
+    // bytes arriving per column: cs candidates (row + key + row index) + row c
+    L.col_bytes = (unsigned)cs * (PNB * 8 + 16) + PNB * 8;
+    L.dbg_on = a.dbg && me == 0 && tid == 0;
+    L.u_prev = 0.0;
+    L.info_col = -1;
+    {
+        double c0[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) c0[q] = r[q][0];
+        panel_push<R>(r, c0, myrow, 0, sm, cl, cs, me, 0 >= rbeg && 0 < rend);
+    }
+    static_assert(PNB == 4 * PKB, "four column blocks");
+    panel_cols<R, 0>(r, myrow, sm, cl, L);
+    if (nb > PKB) panel_cols<R, PKB>(r, myrow, sm, cl, L);
+    if (nb > 2 * PKB) panel_cols<R, 2 * PKB>(r, myrow, sm, cl, L);
+    if (nb > 3 * PKB) panel_cols<R, 3 * PKB>(r, myrow, sm, cl, L);
     cl.sync();  // no CTA may exit while others may still write its shared memory
     if (me == 0 && tid == 0) {
         for (int k = 0; k < nb; ++k) a.piv[a.j0 + k] = a.j0 + sm.piv[k];
-        if (info_col >= 0 && *a.info == 0) *a.info = (int32_t)(a.j0 + info_col + 1);
-        if (dbg_on)
+        if (L.info_col >= 0 && *a.info == 0) *a.info = (int32_t)(a.j0 + L.info_col + 1);
+        if (L.dbg_on)
             for (int k = 0; k < 8 * nb; ++k) a.dbg[k] = sm.dclk[k];
     }
 #pragma unroll

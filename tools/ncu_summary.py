@@ -7,8 +7,8 @@ import sys
 
 WANT = {
     "gpu__time_duration.sum": "us",
-    "dram__bytes_read.sum": "dram_rd",
-    "dram__bytes_write.sum": "dram_wr",
+    "dram__bytes_read.sum": "dram_rd_MB",
+    "dram__bytes_write.sum": "dram_wr_MB",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram%",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm%",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "occ%",
@@ -45,10 +45,13 @@ def main(path):
         d = dict(zip(hdr, r))
         name = re.sub(r"\(.*", "", d.get("Kernel Name", ""))[:70]
         vals = {}
+        unit_of = dict(zip(hdr, units))
+        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,  # -> us
+                 "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}          # -> MB
         for k, short in WANT.items():
             if k in d and d[k] not in ("", "n/a"):
                 try:
-                    vals[short] = float(d[k].replace(",", ""))
+                    vals[short] = float(d[k].replace(",", "")) * scale.get(unit_of.get(k, ""), 1.0)
                 except ValueError:
                     pass
         stalls = sorted(((v, k) for k, v in vals.items() if k.startswith("st_")), reverse=True)[:5]
