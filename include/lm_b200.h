@@ -150,6 +150,14 @@ int lm_set_identity(int dtype, lm_view out, void *stream);
  * d_info[b] = 0 or failing column + 1. */
 int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void *x, void *lu_out, int64_t *d_piv,
                         int32_t *d_info, void *stream);
+/* lm_lu_solve_batched plus, in the same pass, each instance's R10 structure
+ * class (rewrite.py:146-173 over _analyze): d_cls[b] = 0 general, 1 band
+ * (lbw + ubw <= max(4, n/4)), 2 upper triangular, 3 lower triangular,
+ * 4 symmetric.  Every instance is LU-solved; the caller re-solves the
+ * band / triangular ones with their own kernels (their LU result and
+ * d_info entry are not meaningful).  One kernel, one host read. */
+int lm_solve_batched_classified(int dtype, int64_t n, int64_t batch, const void *a, void *x, int32_t *d_cls,
+                                int32_t *d_info, void *stream);
 /* Batched structure classification of `batch` contiguous F-order n x n
  * matrices: d_out[3*b + {0,1,2}] = lbw, ubw, sym. */
 int lm_analyze_batched(int dtype, int64_t n, int64_t batch, const void *a, int64_t *d_out, void *stream);

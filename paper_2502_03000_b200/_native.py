@@ -33,7 +33,7 @@ EXPORTS = (
     "lm_diag_scale", "lm_diag_of_product", "lm_trace_of_product", "lm_triple_diag_dot",
     "lm_analyze", "lm_lu_factor", "lm_lu_solve", "lm_band_solve", "lm_tri_solve",
     "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
-    "lm_lu_solve_batched", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
+    "lm_lu_solve_batched", "lm_solve_batched_classified", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
     "lm_debug_lu_panel",
 )
 
@@ -73,6 +73,7 @@ _SIGS = {
     "lm_diag_materialise": (_i, [_i, Vec, View, _p]),
     "lm_set_identity": (_i, [_i, View, _p]),
     "lm_lu_solve_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p]),
+    "lm_solve_batched_classified": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p]),
     "lm_analyze_batched": (_i, [_i, _i64, _i64, _p, _p, _p]),
     "lm_expr_atb_schur_trace_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "lm_fill_uniform": (_i, [_i, View, ctypes.c_uint64, _i64, _i64, _i64, _d, _d, _p]),

@@ -6,13 +6,13 @@ evaluate a batch of same-shaped instances with ONE kernel per plan step
 instead of one Python evaluate per instance, with per-instance results
 identical to evaluating every instance on its own:
 
-* ``solve_batched(A, b)``: inverse(A_i)*b_i (BASELINE config 4b).  The
-  per-instance R9/R10 structure dispatch (lazymat/rewrite.py:389-414) runs
-  as one batched device scan; instances whose plan is ``lu_solve`` (the
-  general and symmetric classes) are solved by one in-shared-memory LU
-  kernel in the reference's exact operation order -- values and pivots
-  bit-identical to per-instance lazymat.  Band / triangular instances go
-  through the single-instance planner.
+* ``solve_batched(A, b)``: inverse(A_i)*b_i (BASELINE config 4b).  One
+  kernel classifies every instance with the R9/R10 structure ladder
+  (lazymat/rewrite.py:389-414) and solves it with a register-resident LU
+  in the reference's exact operation order -- values and pivots
+  bit-identical to per-instance lazymat -- and the host reads (class,
+  info) once.  Band / triangular instances are then re-solved through the
+  single-instance planner (their plan is not lu_solve).
 * ``atb_schur_trace(A, B, C, D)``: E_i = A_i.T*B_i + C_i % D_i and
   s_i = trace(A_i*B_i) (BASELINE config 5a), one fused kernel per size
   class that reads every operand once.
@@ -112,22 +112,28 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
     bt, n, n2 = A.shape
     if n != n2 or b.shape[1] != n or b.shape[2] != 1:
         raise KernelContractError("solve_batched: A must be (batch, n, n) and b (batch, n, 1)")
-    info = analyze_batched(A)
-    band, triu, tril, symm = _classify(info, n)
-    cls = np.zeros(bt, dtype=np.int8)
-    cls[symm] = 4
-    cls[tril] = 3
-    cls[triu] = 2
-    cls[band] = 1
-    lu_mask = (cls == 0) | (cls == 4)
     x = torch.empty((bt, 1, n), dtype=A.dtype, device=A.device).transpose(1, 2)
     x.copy_(b)
-    if lu_mask.all() and n <= 64:
-        dinfo = torch.empty(bt, dtype=torch.int32, device=A.device)
-        N.call("lm_lu_solve_batched", N.dtype_code(A), n, bt, A.data_ptr(), x.data_ptr(), None, None,
-               dinfo.data_ptr())
+    if n <= 64 and A.dtype == torch.float64:
+        # one kernel: structure class + exact LU solve of every instance; one
+        # host read of (class, info)
+        ci = torch.empty(2 * bt, dtype=torch.int32, device=A.device)
+        N.call("lm_solve_batched_classified", N.dtype_code(A), n, bt, A.data_ptr(), x.data_ptr(), ci.data_ptr(),
+               ci.data_ptr() + 4 * bt)
+        host = ci.cpu().numpy()
+        cls, hinfo = host[:bt].astype(np.int8), host[bt:]
+    else:
+        info = analyze_batched(A)
+        band, triu, tril, symm = _classify(info, n)
+        cls = np.zeros(bt, dtype=np.int8)
+        cls[symm] = 4
+        cls[tril] = 3
+        cls[triu] = 2
+        cls[band] = 1
+        hinfo = None
+    lu_mask = (cls == 0) | (cls == 4)
+    if hinfo is not None and lu_mask.all():
         if check:
-            hinfo = dinfo.cpu().numpy()
             bad = np.flatnonzero(hinfo)
             if bad.size:
                 i = int(bad[0])
@@ -135,10 +141,17 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
                 raise SingularMatrixError(f"singular matrix in instance {i}: zero pivot in column {col}",
                                           column=col)
         return BatchSolveResult(x, cls)
-    # mixed classes (or n > 64): the single-instance planner per instance
+    # mixed classes (or n > 64): instances in index order; LU-class ones
+    # were solved above, the others take the single-instance planner
     from .expr import inverse
     from .rewrite import evaluate
     for i in range(bt):
+        if hinfo is not None and lu_mask[i]:
+            if check and hinfo[i]:
+                col = int(hinfo[i]) - 1
+                raise SingularMatrixError(f"singular matrix in instance {i}: zero pivot in column {col}",
+                                          column=col)
+            continue
         ai = DenseMatrix(A[i])
         bi = DenseMatrix(b[i])
         x[i].copy_(evaluate(inverse(ai) * bi).data)

@@ -22,10 +22,11 @@
 
 namespace lm {
 
-template <int N>
+template <int N, bool CLASSIFY>
 __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, const double *__restrict__ A,
                                                      double *__restrict__ X, double *__restrict__ LU,
-                                                     int64_t *__restrict__ piv, int32_t *__restrict__ info) {
+                                                     int64_t *__restrict__ piv, int32_t *__restrict__ info,
+                                                     int32_t *__restrict__ cls) {
     constexpr int W = N / 32 > 0 ? N / 32 : 1;  // warps per system
     constexpr unsigned MASK = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
     __shared__ double cand_row[2][W][N];        // published candidate rows (double-buffered by k parity)
@@ -48,6 +49,54 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
     double xv = t < n ? __ldg(X + b * n + t) : 0.0;
     int pos = t;  // current position of the row this thread owns
     if (t == 0) s_fail = 0;
+    if constexpr (CLASSIFY) {
+        // the R10 structure ladder of this instance (lazymat/rewrite.py:146-173
+        // over _analyze, lazymat/_loops.py:15-34), from the registers: lower /
+        // upper bandwidth over nonzeros, exact symmetry through a transposed
+        // shared-memory copy
+        __shared__ double sAt[N][N + 1];
+        __shared__ unsigned s_lb[W], s_ub[W], s_as[W];
+        unsigned lb = 0, ub = 0, asym = 0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (t < n && j < n) {
+                sAt[t][j] = r[j];
+                if (r[j] != 0.0) {
+                    if (t > j) lb = max(lb, (unsigned)(t - j));
+                    if (j > t) ub = max(ub, (unsigned)(j - t));
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (t < n && j < n && j > t && !(r[j] == sAt[j][t])) asym = 1;
+        constexpr unsigned MASK = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
+        lb = __reduce_max_sync(MASK, lb);
+        ub = __reduce_max_sync(MASK, ub);
+        asym = __reduce_or_sync(MASK, asym);
+        if ((t & 31) == 0) {
+            s_lb[t >> 5] = lb;
+            s_ub[t >> 5] = ub;
+            s_as[t >> 5] = asym;
+        }
+        __syncthreads();
+        if (t == 0) {
+#pragma unroll
+            for (int q = 1; q < W; ++q) {
+                lb = max(lb, s_lb[q]);
+                ub = max(ub, s_ub[q]);
+                asym |= s_as[q];
+            }
+            const unsigned lim = (unsigned)(n / 4 > 4 ? n / 4 : 4);
+            int c = 0;  // general
+            if (lb + ub <= lim) c = 1;        // band
+            else if (lb == 0) c = 2;          // upper triangular
+            else if (ub == 0) c = 3;          // lower triangular
+            else if (!asym) c = 4;            // symmetric (still LU)
+            cls[b] = c;
+        }
+    }
     __syncthreads();
 
 #pragma unroll
@@ -150,6 +199,19 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
 
 using namespace lm;
 
+template <bool CLASSIFY>
+static int launch_batched(int64_t n, int64_t batch, const double *A, double *X, double *LU, int64_t *d_piv,
+                          int32_t *d_info, int32_t *d_cls, cudaStream_t s) {
+    if (n <= 16)
+        lu_batched_rows<16, CLASSIFY><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
+    else if (n <= 32)
+        lu_batched_rows<32, CLASSIFY><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
+    else
+        lu_batched_rows<64, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
 extern "C" int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void *x, void *lu_out,
                                    int64_t *d_piv, int32_t *d_info, void *stream) {
     clear_error();
@@ -157,15 +219,17 @@ extern "C" int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const vo
     LM_REQUIRE(n >= 1 && n <= 64, "lu_solve_batched: 1 <= n <= 64 (got %lld)", (long long)n);
     if (batch == 0) return 0;
     LM_REQUIRE(batch <= 0x7fffffff, "lu_solve_batched: batch too large");
-    cudaStream_t s = as_stream(stream);
-    const double *A = (const double *)a;
-    double *X = (double *)x, *LU = (double *)lu_out;
-    if (n <= 16)
-        lu_batched_rows<16><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, LU, d_piv, d_info);
-    else if (n <= 32)
-        lu_batched_rows<32><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, LU, d_piv, d_info);
-    else
-        lu_batched_rows<64><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, LU, d_piv, d_info);
-    LM_LAUNCHED(1);
-    return 0;
+    return launch_batched<false>(n, batch, (const double *)a, (double *)x, (double *)lu_out, d_piv, d_info, nullptr,
+                                 as_stream(stream));
+}
+
+extern "C" int lm_solve_batched_classified(int dtype, int64_t n, int64_t batch, const void *a, void *x,
+                                           int32_t *d_cls, int32_t *d_info, void *stream) {
+    clear_error();
+    LM_REQUIRE(dtype == LM_F64, "solve_batched_classified: f64 only");
+    LM_REQUIRE(n >= 1 && n <= 64, "solve_batched_classified: 1 <= n <= 64 (got %lld)", (long long)n);
+    if (batch == 0) return 0;
+    LM_REQUIRE(batch <= 0x7fffffff, "solve_batched_classified: batch too large");
+    return launch_batched<true>(n, batch, (const double *)a, (double *)x, nullptr, nullptr, d_info, d_cls,
+                                as_stream(stream));
 }

@@ -83,3 +83,40 @@ def test_atb_schur_trace_vs_oracle(n, dtype):
         assert np.max(np.abs(E[i] - Er)) <= tol * max(np.max(np.abs(Er)), 1e-30)
         tr = O.trace_of_product(A, B)
         assert abs(s[i] - tr) <= tol * max(abs(tr), np.sum(np.abs(A * B.T)) * 1e-2)
+
+
+@pytest.mark.parametrize("n", [1, 3, 5, 16, 33, 64])
+def test_classified_kernel_matches_structure_scan(n):
+    """The one-pass classify+solve kernel assigns every instance the class
+    the batched structure scan + R10 ladder gives."""
+    from paper_2502_03000_b200 import _native as N
+    from paper_2502_03000_b200.batch import _classify, analyze_batched
+
+    rng = np.random.default_rng(100 + n)
+    mats = []
+    for kind in range(12):
+        a = rng.uniform(-1, 1, (n, n)) + n * np.eye(n)
+        if kind % 6 == 1:
+            a = np.triu(np.tril(a, 1), -1)          # tridiagonal (band)
+        elif kind % 6 == 2:
+            a = np.triu(a)
+        elif kind % 6 == 3:
+            a = np.tril(a)
+        elif kind % 6 == 4:
+            a = a + a.T
+        elif kind % 6 == 5:
+            a[rng.integers(0, n), rng.integers(0, n)] = 0.0
+        mats.append(a)
+    A = stack_fortran(np.array(mats))
+    bt = A.shape[0]
+    x = torch.zeros((bt, 1, n), dtype=torch.float64, device=A.device).transpose(1, 2)
+    ci = torch.empty(2 * bt, dtype=torch.int32, device=A.device)
+    N.call("lm_solve_batched_classified", 0, n, bt, A.data_ptr(), x.data_ptr(), ci.data_ptr(), ci.data_ptr() + 4 * bt)
+    got = ci[:bt].cpu().numpy()
+    band, triu, tril, symm = _classify(analyze_batched(A), n)
+    want = np.zeros(bt, dtype=np.int32)
+    want[symm] = 4
+    want[tril] = 3
+    want[triu] = 2
+    want[band] = 1
+    assert np.array_equal(got, want)
