@@ -98,10 +98,10 @@ __global__ void __launch_bounds__(kGvThreads) gemv_colmajor(View<const T> M, Vec
 // variant was no faster: its __threadfence per CTA cost what the second
 // launch does.)
 constexpr int kGv32Warps = 8;
-constexpr int kGv32KC = 64;
-template <class T>
-__global__ void __launch_bounds__(kGv32Warps * 32, 3) gemv_cm32(const T *__restrict__ M, int64_t ld, int64_t p,
-                                                              int64_t q, Vec<const T> x, T *__restrict__ part) {
+template <class T, int KC, int MINB>
+__global__ void __launch_bounds__(kGv32Warps * 32, MINB) gemv_cm32(const T *__restrict__ M, int64_t ld, int64_t p,
+                                                                 int64_t q, Vec<const T> x, T *__restrict__ part) {
+    constexpr int kGv32KC = KC;
     constexpr int RPT = Vec32<T>::N;
     constexpr int RB = 32 * RPT;  // rows per CTA
     constexpr int U = kGv32KC / kGv32Warps;  // columns per warp
@@ -192,15 +192,18 @@ template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_v
     Vec<const T> x{(const T *)xv.ptr, xv.n, xv.stride};
     const int nsm = num_sms();
     constexpr int RPT32 = Vec32<T>::N;
+    // 64-column chunks, 4 CTAs per SM (64 registers, no spill): 5.3 TB/s on
+    // config 3a; 3 CTAs/SM spilled (4.7), 128-column chunks spill (3.0-3.6)
+    constexpr int KCv = 64;
     if (q > 0 && mv.rs == 1 && p % RPT32 == 0 && (mv.cols <= 1 || mv.cs % RPT32 == 0) && aligned32(mv.ptr) &&
-        ceil_div(q, kGv32KC) <= 65535) {
+        ceil_div(q, KCv) <= 65535) {
         constexpr int RB = 32 * RPT32;
-        const int64_t rowblocks = ceil_div(p, RB), chunks = ceil_div(q, kGv32KC);
+        const int64_t rowblocks = ceil_div(p, RB), chunks = ceil_div(q, KCv);
         const int64_t ld = mv.cols > 1 ? mv.cs : p;
         Scratch part;
         if (int rc = part.alloc(sizeof(T) * p * chunks, s)) return rc;
-        gemv_cm32<T><<<dim3((unsigned)rowblocks, (unsigned)chunks), kGv32Warps * 32, 0, s>>>((const T *)mv.ptr, ld, p,
-                                                                                            q, x, part.as<T>());
+        const dim3 grid((unsigned)rowblocks, (unsigned)chunks);
+        gemv_cm32<T, KCv, 4><<<grid, kGv32Warps * 32, 0, s>>>((const T *)mv.ptr, ld, p, q, x, part.as<T>());
         gemv_finish<T><<<(unsigned)ceil_div(p, 32), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
         LM_LAUNCHED(2);
         return 0;
