@@ -203,7 +203,7 @@ template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_v
         Scratch part;
         if (int rc = part.alloc(sizeof(T) * p * chunks, s)) return rc;
         const dim3 grid((unsigned)rowblocks, (unsigned)chunks);
-        gemv_cm32<T, KCv, 4><<<grid, kGv32Warps * 32, 0, s>>>((const T *)mv.ptr, ld, p, q, x, part.as<T>());
+        gemv_cm32<T, KCv, sizeof(T) == 8 ? 4 : 3><<<grid, kGv32Warps * 32, 0, s>>>((const T *)mv.ptr, ld, p, q, x, part.as<T>());
         gemv_finish<T><<<(unsigned)ceil_div(p, 32), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
         LM_LAUNCHED(2);
         return 0;
