@@ -13,6 +13,10 @@
 // per block instead of ~500 dependent kernel launches.
 #include <cooperative_groups.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -164,9 +168,190 @@ __global__ void __launch_bounds__(WT, 1) lu_solve_wave(WaveArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// v2: right-hand sides split into groups of 32 -- the groups are independent
+// solves, so CTA (I, g) handles rows [64I, 64I+64) x columns [32g, 32g+32)
+// and waits only on the flags of its own group.  The wavefront's critical
+// path per block (the last block's contribution + the triangle) shrinks by
+// the group count: one contribution is 64x64x16 exact MACs instead of
+// 64x64x64 on one SM, and the diagonal tile is staged once per sweep.
+// Triangle: 8 lanes per right-hand side, lane g owns rows g, g+8, ...;
+// x_j is broadcast with an 8-wide shuffle.
+constexpr int G2 = 32;        // right-hand sides per group
+constexpr int G2LD = G2 + 1;
+constexpr int LPR = WT / G2;    // triangle: lanes per right-hand side (8)
+constexpr int RPL = WB / LPR;   // rows per lane (8)
+constexpr int APT = WB * G2 / WT;  // accumulation outputs per thread (8)
+
+struct Wave2Args {
+    const double *LU;
+    int64_t lda, n;
+    double *X;
+    int64_t ldx;
+    int m, nblk, ngrp;
+    int *flags;  // [2][nblk][ngrp], zeroed
+    unsigned long long *dbg;  // optional: [2][nblk] globaltimer at each flag raise (group 0)
+};
+
+__global__ void __launch_bounds__(WT, 2) lu_solve_wave2(Wave2Args a) {
+    extern __shared__ double sw2[];
+    double *sL = sw2;              // [WB][WLD]: off-diagonal tile L[i0.., j0..]
+    double *sD = sL + WB * WLD;    // [WB][WLD]: this block's diagonal tile (staged once per sweep)
+    double *sX = sD + WB * WLD;    // [WB][G2LD]: sX[j][c]
+    double *sY = sX + WB * G2LD;   // [WB][G2LD]: this block's rows
+    cg::grid_group grid = cg::this_grid();
+    const int I = blockIdx.x / a.ngrp, g = blockIdx.x - I * a.ngrp, tid = threadIdx.x;
+    const int64_t i0 = (int64_t)I * WB;
+    const int c0 = g * G2;
+    const int mg = (a.m - c0) < G2 ? (a.m - c0) : G2;
+    const int rows = (int)((a.n - i0) < WB ? (a.n - i0) : WB);
+    const int cc = tid % G2, rr = tid / G2;  // accumulation: column cc, rows rr + (WT/G2) q
+    constexpr int RS = WT / G2;              // row step of the accumulation (8)
+    for (int sweep = 0; sweep < 2; ++sweep) {
+        const bool fwd = sweep == 0;
+        int *flags = a.flags + (int64_t)sweep * a.nblk * a.ngrp;
+        // the diagonal tile never changes: off the critical path
+        for (int e = tid; e < WB * WB; e += WT) {
+            const int i = e % WB, j = e / WB;
+            sD[i * WLD + j] = (i < rows && j < rows) ? a.LU[(i0 + i) + (i0 + j) * a.lda] : 0.0;
+        }
+        double acc[APT];
+#pragma unroll
+        for (int q = 0; q < APT; ++q) {
+            const int i = rr + RS * q;
+            acc[q] = (i < rows && cc < mg) ? a.X[(i0 + i) + (int64_t)(c0 + cc) * a.ldx] : 0.0;
+        }
+        const int nJ = fwd ? I : a.nblk - 1 - I;
+        for (int t = 0; t < nJ; ++t) {
+            const int J = fwd ? t : a.nblk - 1 - t;
+            const int64_t j0 = (int64_t)J * WB;
+            const int cols = (int)((a.n - j0) < WB ? (a.n - j0) : WB);
+            for (int e = tid; e < WB * WB; e += WT) {
+                const int i = e % WB, j = e / WB;
+                sL[i * WLD + j] = (i < rows && j < cols) ? a.LU[(i0 + i) + (j0 + j) * a.lda] : 0.0;
+            }
+            wait_flag(flags + (int64_t)J * a.ngrp + g);
+            for (int e = tid; e < WB * G2; e += WT) {
+                const int j = e % WB, c = e / WB;
+                sX[j * G2LD + c] = (j < cols && c < mg) ? a.X[(j0 + j) + (int64_t)(c0 + c) * a.ldx] : 0.0;
+            }
+            __syncthreads();
+            if (cols == WB) {
+#pragma unroll 8
+                for (int q2 = 0; q2 < WB; ++q2) {
+                    const int j = fwd ? q2 : WB - 1 - q2;
+                    const double xv = sX[j * G2LD + cc];
+#pragma unroll
+                    for (int q = 0; q < APT; ++q)
+                        acc[q] = __dsub_rn(acc[q], __dmul_rn(sL[(rr + RS * q) * WLD + j], xv));
+                }
+            } else {
+                for (int q2 = 0; q2 < cols; ++q2) {
+                    const int j = fwd ? q2 : cols - 1 - q2;
+                    const double xv = sX[j * G2LD + cc];
+#pragma unroll
+                    for (int q = 0; q < APT; ++q)
+                        acc[q] = __dsub_rn(acc[q], __dmul_rn(sL[(rr + RS * q) * WLD + j], xv));
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < APT; ++q) sY[(rr + RS * q) * G2LD + cc] = acc[q];
+        __syncthreads();
+        {
+            // LPR lanes per right-hand side: c = tid / LPR, lane gl owns rows gl + LPR r
+            const int c = tid / LPR, gl = tid % LPR;
+            double x[RPL];
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) x[r] = sY[(gl + LPR * r) * G2LD + c];
+            if (fwd) {
+#pragma unroll
+                for (int j = 0; j < WB; ++j) {
+                    if (j >= rows) break;
+                    const double xj = __shfl_sync(0xffffffffu, x[j / LPR], j % LPR, LPR);
+#pragma unroll
+                    for (int r = 0; r < RPL; ++r) {
+                        const int i = gl + LPR * r;
+                        if (i > j && i < rows) x[r] = __dsub_rn(x[r], __dmul_rn(sD[i * WLD + j], xj));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = WB - 1; j >= 0; --j) {
+                    if (j >= rows) continue;
+                    if (gl == j % LPR) x[j / LPR] = __ddiv_rn(x[j / LPR], sD[j * WLD + j]);
+                    const double xj = __shfl_sync(0xffffffffu, x[j / LPR], j % LPR, LPR);
+#pragma unroll
+                    for (int r = 0; r < RPL; ++r) {
+                        const int i = gl + LPR * r;
+                        if (i < j) x[r] = __dsub_rn(x[r], __dmul_rn(sD[i * WLD + j], xj));
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < RPL; ++r) sY[(gl + LPR * r) * G2LD + c] = x[r];
+        }
+        __syncthreads();
+        for (int e = tid; e < WB * G2; e += WT) {
+            const int i = e % WB, c = e / WB;
+            if (i < rows && c < mg) a.X[(i0 + i) + (int64_t)(c0 + c) * a.ldx] = sY[i * G2LD + c];
+        }
+        raise_flag(flags + (int64_t)I * a.ngrp + g);
+        if (a.dbg && g == 0 && tid == 0) {
+            unsigned long long tt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+            a.dbg[sweep * a.nblk + I] = tt;
+        }
+        if (fwd) grid.sync();  // every row final before the back sweep reads any
+    }
+}
+
+static int lu_solve_wavefront2(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m,
+                               cudaStream_t s) {
+    const int nblk = (int)ceil_div(n, WB), ngrp = (int)ceil_div(m, G2);
+    const size_t smem = sizeof(double) * (2 * WB * WLD + 2 * WB * G2LD);
+    static bool attr = false;
+    if (!attr) {
+        LM_CUDA(cudaFuncSetAttribute(lu_solve_wave2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    int per_sm = 0;
+    LM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_solve_wave2, WT, smem));
+    if ((int64_t)per_sm * num_sms() < (int64_t)nblk * ngrp) return 1;
+    Scratch flags;
+    const size_t fb = sizeof(int) * 2 * (size_t)nblk * ngrp;
+    if (int rc = flags.alloc(fb, s)) return rc;
+    LM_CUDA(cudaMemsetAsync(flags.p, 0, fb, s));
+    static unsigned long long *dbg = nullptr;
+    static bool want = getenv("LM_SOLVE_TRACE") != nullptr;
+    if (want && !dbg) LM_CUDA(cudaMalloc(&dbg, sizeof(unsigned long long) * 2 * 4096));
+    Wave2Args args{LU, lda, n, X, ldx, (int)m, nblk, ngrp, flags.as<int>(), want && nblk <= 2048 ? dbg : nullptr};
+    void *kargs[] = {&args};
+    LM_CUDA(cudaLaunchCooperativeKernel((const void *)lu_solve_wave2, dim3(nblk * ngrp), dim3(WT), kargs, smem, s));
+    count_launch(1);
+    if (args.dbg) {
+        std::vector<unsigned long long> h(2 * nblk);
+        cudaStreamSynchronize(s);
+        cudaMemcpy(h.data(), dbg, sizeof(unsigned long long) * 2 * nblk, cudaMemcpyDeviceToHost);
+        unsigned long long t0 = h[0];
+        for (int i = 0; i < 2 * nblk; ++i) t0 = h[i] < t0 ? h[i] : t0;
+        for (int sw = 0; sw < 2; ++sw)
+            for (int i = 0; i < nblk; i += (nblk / 16 > 0 ? nblk / 16 : 1))
+                fprintf(stderr, "SOLVETRACE sweep %d block %4d flag at %8.1f us\n", sw, i,
+                        (h[sw * nblk + i] - t0) / 1e3);
+    }
+    return 0;
+}
+
 // 0 = done; 1 = not applicable (caller uses the launch-per-block path)
 int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s) {
-    if (m < 1 || m > WM || n < 1) return 1;
+    if (m < 1 || n < 1) return 1;
+    if (m > G2) {  // several right-hand-side groups: independent wavefronts
+        const int rc = lu_solve_wavefront2(LU, n, lda, X, ldx, m, s);
+        if (rc != 1) return rc;
+    }
+    if (m > WM) return 1;
     const int nblk = (int)ceil_div(n, WB);
     const size_t smem = sizeof(double) * 3 * WB * WLD;
     static bool attr = false;

@@ -382,6 +382,22 @@ def test_lu_factor_large_general_bitwise(n):
     assert bits_equal(host(x), x_ref)
 
 
+@pytest.mark.parametrize("n,m", [(300, 17), (700, 40), (700, 64), (257, 100)])
+def test_lu_solve_rhs_groups_bitwise(n, m):
+    """More than 16 right-hand sides: independent 16-column wavefronts
+    (partial last group, more groups than the one-group kernel's limit)."""
+    rng = np.random.default_rng(n * 7 + m)
+    a = np.asfortranarray(rng.uniform(-1, 1, (n, n)))
+    rc, lu_ref, piv_ref = O.lu_factor(a)
+    assert rc == 0
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, m)))
+    x_ref = np.array(b, order="F")
+    O.lu_solve(lu_ref, piv_ref, x_ref)
+    x = dev(np.array(b, order="F"))
+    lm.kernels.lu_solve_into(dev(a), x)
+    assert bits_equal(host(x), x_ref)
+
+
 @pytest.mark.slow
 def test_config4a_full_size_residual_and_pivots():
     """BASELINE config 4a at full size: A = U(-1,1) + 8192 I, b 8192 x 64."""
