@@ -9,9 +9,18 @@ import random
 LEAF_SHAPES = [(4, 4), (4, 1), (1, 4), (1, 1), (4, 3), (3, 4), (3, 3), (3, 1)]
 
 
+def _values(r, c):
+    """Seeded U(-1,1) values (column-major), square leaves boosted by 4 on
+    the diagonal so inverses and solves are well defined."""
+    import numpy as np
+    v = np.random.default_rng(10 * r + c).uniform(-1.0, 1.0, (r, c))
+    if r == c:
+        v = v + 4.0 * np.eye(r)
+    return [float(x) for x in v.flatten(order="F")]
+
+
 def leaves(api):
-    return [api.make_matrix(r, c, fill="values", values=[float(k + 1) for k in range(r * c)])
-            for r, c in LEAF_SHAPES]
+    return [api.make_matrix(r, c, fill="values", values=_values(r, c)) for r, c in LEAF_SHAPES]
 
 
 def build(api, mats, rng: random.Random, depth: int):
@@ -44,13 +53,28 @@ def build(api, mats, rng: random.Random, depth: int):
     return api.row_of(a, rng.randrange(5))
 
 
-def record(api, n_trees: int = 400, seed: int = 2025):
-    """[(render, shape-or-error)] for n_trees seeded trees."""
+def trees(api, n_trees: int = 400, seed: int = 2025):
     rng = random.Random(seed)
     mats = leaves(api)
+    return [build(api, mats, rng, rng.randrange(1, 5)) for _ in range(n_trees)]
+
+
+def value_record(api, t):
+    """The evaluate() result as a flat column-major list (or [float]), or
+    the error type name."""
+    try:
+        v = api.evaluate(t)
+    except Exception as e:  # noqa: BLE001
+        return ["error", type(e).__name__]
+    if isinstance(v, float):
+        return ["ok", [v]]
+    return ["ok", [float(x) for x in v.to_values()]]
+
+
+def record(api, n_trees: int = 400, seed: int = 2025):
+    """[(render, shape-or-error)] for n_trees seeded trees."""
     out = []
-    for _ in range(n_trees):
-        t = build(api, mats, rng, rng.randrange(1, 5))
+    for t in trees(api, n_trees, seed):
         try:
             sh = api.validate(t)
             ish = api.infer_shape(t)

@@ -18,9 +18,11 @@ sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, str(HERE))
 
 import lazymat  # noqa: E402
-from fuzz_trees import record  # noqa: E402
+from fuzz_trees import record, trees, value_record  # noqa: E402
 
 if __name__ == "__main__":
     rec = record(lazymat)
-    (HERE / "fuzz_trees.json").write_text(json.dumps(rec, indent=0))
-    print("wrote", len(rec), "trees;", sum(r[1][0] == "error" for r in rec), "errors")
+    vals = [value_record(lazymat, t) if r[1][0] == "ok" else None for t, r in zip(trees(lazymat), rec)]
+    (HERE / "fuzz_trees.json").write_text(json.dumps({"trees": rec, "values": vals}, indent=0))
+    print("wrote", len(rec), "trees;", sum(r[1][0] == "error" for r in rec), "errors;",
+          sum(1 for v in vals if v and v[0] == "error"), "evaluation errors")
