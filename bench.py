@@ -241,6 +241,33 @@ class Config1(Workload):
     def work_per_step(self):
         return 4 * self.N * self.N * 8
 
+    def e2e_fn(self, lm, h):
+        """Through the public API, pipelined over column chunks: each chunk's
+        result streams back to the host while the next chunk's operands are
+        still arriving."""
+        import torch
+        from paper_2502_03000_b200.matrix import MatrixView
+
+        def pin(a):
+            return torch.from_numpy(np.ascontiguousarray(a.T)).pin_memory().t()
+        p = {k: pin(h[k]) for k in "ABC"}
+        n, K = self.N, 8
+        w = n // K
+        out = torch.empty((n, n), dtype=torch.float64).pin_memory().t()
+
+        def run():
+            dev = {k: lm.empty_matrix(n, n) for k in "ABC"}
+            fs = []
+            for c in range(K):
+                for k in "ABC":
+                    lm.upload_into(dev[k], p[k][:, c * w:(c + 1) * w], c * w)
+                A, B, C = (MatrixView(dev[k], 0, c * w, n, w) for k in "ABC")
+                fs.append(lm.download(lm.evaluate(2 * A + B % C - A / (1 + abs(B))), out=out[:, c * w:(c + 1) * w]))
+            for f in fs:
+                f.wait()
+            return [out]
+        return run, 3 * n * n * 8, n * n * 8
+
     def kernels_for_roofline(self, lm, m):
         from paper_2502_03000_b200 import kernels as K
         from paper_2502_03000_b200.matrix import fortran_empty
