@@ -483,10 +483,25 @@ class Config4b(Workload):
         pb = torch.from_numpy(np.ascontiguousarray(h["b"])).pin_memory()
         px = torch.empty_like(pb).pin_memory()
 
+        K = 4  # instance chunks: chunk k is solved while chunks > k are still uploading
+        bt = self.BATCH
+        bk = bt // K
+        h2d = torch.cuda.Stream()
+
         def run():
-            A = pa.cuda(non_blocking=True).transpose(1, 2)
-            x = solve_batched(A, pb.cuda(non_blocking=True)).x
-            px.copy_(x)
+            chunks = []
+            h2d.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(h2d):
+                for k in range(K):
+                    A = pa[k * bk:(k + 1) * bk].cuda(non_blocking=True).transpose(1, 2)
+                    b = pb[k * bk:(k + 1) * bk].cuda(non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(h2d)
+                    chunks.append((A, b, ev))
+            for k, (A, b, ev) in enumerate(chunks):
+                torch.cuda.current_stream().wait_event(ev)
+                x = solve_batched(A, b).x
+                px[k * bk:(k + 1) * bk].copy_(x, non_blocking=True)
             torch.cuda.synchronize()
             return [px]
         return run, pa.numel() * 8 + pb.numel() * 8, px.numel() * 8
