@@ -39,6 +39,7 @@ class CapturedPlan:
         if not torch.cuda.is_available():
             raise BackendUnavailableError("CUDA-graph capture needs a CUDA device")
         self.plan = plan
+        torch.cuda.synchronize()  # pending uploads of the leaves (transfer.upload) have landed
         for _ in range(warmup):
             execute(plan, host_scalar=False)
         torch.cuda.synchronize()
