@@ -161,7 +161,33 @@ __global__ void __launch_bounds__(2 * N) atb_schur_trace_tc(int64_t batch, const
         // epilogue: E = round(acc) + round(C * D)
         const T *pc = C + b * nn, *pd = D + b * nn;
         T *pe = E + b * nn;
-        if constexpr (sizeof(T) == 8) {
+        if constexpr (sizeof(T) == 8 && N <= 64) {
+            // stage the product tile through the (now idle) A/B buffers, then
+            // one coalesced 32-byte pass over C, D and E
+            constexpr int LDE = N + 1;
+            double *st = reinterpret_cast<double *>(&sm.a[0][0]);
+            static_assert(sizeof(sm.a) + sizeof(sm.b) >= sizeof(double) * N * LDE, "staging fits");
+            const int wm = (warp % (N / 32)) * 32, wn = (warp / (N / 32)) * WTN;
+            const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        st[(wn + j * 8 + 2 * fc + h) * LDE + wm + i * 8 + fr] = acc[i][j][h];
+            __syncthreads();
+            constexpr int NV = N * N / 4;  // 32-byte vectors per instance
+#pragma unroll
+            for (int v = tid; v < NV; v += NT) {
+                const int e = v * 4, n = e / N, m = e - n * N;
+                const Vec32<double> cv = ld_stream32(pc + e), dv = ld_stream32(pd + e);
+                Vec32<double> ev;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) ev.v[l] = radd(st[n * LDE + m + l], rmul(cv.v[l], dv.v[l]));
+                st_stream32(pe + e, ev);
+            }
+        } else if constexpr (sizeof(T) == 8) {
             const int wm = (warp % (N / 32)) * 32, wn = (warp / (N / 32)) * WTN;
             const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
@@ -174,6 +200,28 @@ __global__ void __launch_bounds__(2 * N) atb_schur_trace_tc(int64_t batch, const
                         const int64_t idx = m + (int64_t)n * N;
                         pe[idx] = radd(acc[i][j][h], rmul(__ldg(pc + idx), __ldg(pd + idx)));
                     }
+        } else if constexpr (N <= 64) {
+            // f32: the same staged, coalesced epilogue (8 floats per vector)
+            constexpr int TR = N / 8;
+            constexpr int LDE = N + 1;
+            float *st = reinterpret_cast<float *>(&sm.a[0][0]);
+            static_assert(sizeof(sm.a) + sizeof(sm.b) >= sizeof(float) * N * LDE, "staging fits");
+            const int trw = tid % TR, tcl = tid / TR;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < N / 16; ++j) st[(tcl + 16 * j) * LDE + trw + TR * i] = facc[i][j];
+            __syncthreads();
+            constexpr int NV = N * N / 8;
+#pragma unroll
+            for (int v = tid; v < NV; v += NT) {
+                const int e = v * 8, n = e / N, m = e - n * N;
+                const Vec32<float> cv = ld_stream32(pc + e), dv = ld_stream32(pd + e);
+                Vec32<float> ev;
+#pragma unroll
+                for (int l = 0; l < 8; ++l) ev.v[l] = radd(st[n * LDE + m + l], rmul(cv.v[l], dv.v[l]));
+                st_stream32(pe + e, ev);
+            }
         } else {
             constexpr int TR = N / 8;
             const int trw = tid % TR, tcl = tid / TR;
@@ -317,6 +365,11 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_half(int64_t batch, co
         const T *pc = C + b * nn, *pd = D + b * nn;
         T *pe = E + b * nn;
         if constexpr (sizeof(T) == 8) {
+            // stage this CTA's 128 x 64 product through the idle staging
+            // buffers, then one coalesced 32-byte pass over C, D and E
+            constexpr int LDE = HN + 1;
+            double *st = reinterpret_cast<double *>(&sm.a[0][0]);
+            static_assert(sizeof(sm.a) + sizeof(sm.b) + sizeof(sm.ac) >= sizeof(double) * HH * LDE, "fits");
             const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
             const int fr = lane >> 2, fc = lane & 3;
 #pragma unroll
@@ -324,11 +377,20 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_half(int64_t batch, co
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int m = wm + i * 8 + fr, n = h * HH + wn + j * 8 + 2 * fc + q;
-                        const int64_t idx = m + (int64_t)n * HN;
-                        pe[idx] = radd(acc[i][j][q], rmul(__ldg(pc + idx), __ldg(pd + idx)));
-                    }
+                    for (int q = 0; q < 2; ++q)
+                        st[(wn + j * 8 + 2 * fc + q) * LDE + wm + i * 8 + fr] = acc[i][j][q];
+            __syncthreads();
+            constexpr int NV = HN * HH / 4;
+#pragma unroll 4
+            for (int v = tid; v < NV; v += 256) {
+                const int e = v * 4, n = e / HN, m = e - n * HN;
+                const int64_t g = (int64_t)(h * HH + n) * HN + m;
+                const Vec32<double> cv = ld_stream32(pc + g), dv = ld_stream32(pd + g);
+                Vec32<double> ev;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) ev.v[l] = radd(st[n * LDE + m + l], rmul(cv.v[l], dv.v[l]));
+                st_stream32(pe + g, ev);
+            }
         } else {
             const int trw = tid & 15, tcl = tid >> 4;
 #pragma unroll
