@@ -133,17 +133,24 @@ __global__ void __launch_bounds__(2 * N) atb_schur_trace_tc(int64_t batch, const
             } else {
                 constexpr int TR = N / 8;  // thread rows
                 const int trw = tid % TR, tcl = tid / TR;  // tcl in [0, 16)
-#pragma unroll 4
-                for (int kl = 0; kl < KC; ++kl) {
-                    float av[8], bv[N / 16];
+                // two k per 8-byte LDS: half the shared-memory wavefronts per FFMA
+                // (the 1-k loop was shared-memory bound at ~50% of FFMA peak)
+#pragma unroll 2
+                for (int kl = 0; kl < KC; kl += 2) {
+                    float2 av[8], bv[N / 16];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) av[i] = as[(trw + TR * i) * LDK + kl];
+                    for (int i = 0; i < 8; ++i) av[i] = *reinterpret_cast<const float2 *>(&as[(trw + TR * i) * LDK + kl]);
 #pragma unroll
-                    for (int j = 0; j < N / 16; ++j) bv[j] = bs[(tcl + 16 * j) * LDK + kl];
+                    for (int j = 0; j < N / 16; ++j)
+                        bv[j] = *reinterpret_cast<const float2 *>(&bs[(tcl + 16 * j) * LDK + kl]);
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int j = 0; j < N / 16; ++j) facc[i][j] = fmaf(av[i], bv[j], facc[i][j]);
+                        for (int j = 0; j < N / 16; ++j) facc[i][j] = fmaf(av[i].x, bv[j].x, facc[i][j]);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < N / 16; ++j) facc[i][j] = fmaf(av[i].y, bv[j].y, facc[i][j]);
                 }
             }
             // trace terms of this chunk: sum_{k in chunk} sum_i A(i,k) * B(k,i)
