@@ -221,7 +221,7 @@ __device__ __forceinline__ void key_first_max(unsigned long long key, int row, b
 template <int R>
 __device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const double (&cv)[R], const int (&myrow)[R],
                                            const int c, PanelSmem &sm, cg::cluster_group &cl, int cs, int me,
-                                           bool own_c) {
+                                           bool own_c, long long *dclk = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int par = c & 1;
     // this thread's best row (rows ascend with q: strict > keeps the first)
@@ -270,7 +270,9 @@ __device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const doub
         sm.wkey[par][wid] = whi == 0 ? 0ull : (((unsigned long long)whi << 32) | wlo);
         sm.wrw[par][wid] = wrow;
     }
+    if (dclk) dclk[4] = clock64();
     __syncthreads();
+    if (dclk) dclk[5] = clock64();
     // the CTA candidate (every warp, redundantly) and the pushes
     unsigned P, who, H, L;
     {
@@ -416,7 +418,8 @@ __device__ __forceinline__ void panel_cols(double (&r)[R][PNB], const int (&myro
         if (L.dbg_on) sm.dclk[kk * 8 + 3] = clock64();
         if (kk + 1 < L.nb) {
             const int c = kk + 1;
-            panel_push<R>(r, cn, myrow, c, sm, cl, L.cs, L.me, c >= L.rbeg && c < L.rend);
+            panel_push<R>(r, cn, myrow, c, sm, cl, L.cs, L.me, c >= L.rbeg && c < L.rend,
+                          L.dbg_on ? &sm.dclk[kk * 8] : nullptr);
         }
         if (L.dbg_on) sm.dclk[kk * 8 + 6] = clock64();
         // the rest of the update while the pushes land
