@@ -306,7 +306,7 @@ __device__ __forceinline__ void panel_push(const double (&r)[R][PNB], const doub
 // kernel is ~21k instructions and stalls on instruction fetch: ncu
 // no_instruction 12 of 20 stall cycles per issue).  Register indices stay
 // static: the j loops start at the block's K0 and predicate on j vs kk.
-constexpr int PKB = 8;
+constexpr int PKB = 4;
 
 struct PanelLoop {
     int cs, me, rbeg, rend, nb;
@@ -481,11 +481,15 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
         for (int q = 0; q < R; ++q) c0[q] = r[q][0];
         panel_push<R>(r, c0, myrow, 0, sm, cl, cs, me, 0 >= rbeg && 0 < rend);
     }
-    static_assert(PNB == 4 * PKB, "four column blocks");
+    static_assert(PNB == 8 * PKB, "eight column blocks");
     panel_cols<R, 0>(r, myrow, sm, cl, L);
     if (nb > PKB) panel_cols<R, PKB>(r, myrow, sm, cl, L);
     if (nb > 2 * PKB) panel_cols<R, 2 * PKB>(r, myrow, sm, cl, L);
     if (nb > 3 * PKB) panel_cols<R, 3 * PKB>(r, myrow, sm, cl, L);
+    if (nb > 4 * PKB) panel_cols<R, 4 * PKB>(r, myrow, sm, cl, L);
+    if (nb > 5 * PKB) panel_cols<R, 5 * PKB>(r, myrow, sm, cl, L);
+    if (nb > 6 * PKB) panel_cols<R, 6 * PKB>(r, myrow, sm, cl, L);
+    if (nb > 7 * PKB) panel_cols<R, 7 * PKB>(r, myrow, sm, cl, L);
     cl.sync();  // no CTA may exit while others may still write its shared memory
     if (me == 0 && tid == 0) {
         for (int k = 0; k < nb; ++k) a.piv[a.j0 + k] = a.j0 + sm.piv[k];
