@@ -268,6 +268,8 @@ int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, dou
                           lda % 2 == 0 && ldb % 2 == 0;
     if (async_ok && N > 32 && ctas(128, 64) >= nsm)  // 45.7 -> 44.0 ms at n = 8192
         return launch_exact_update_c<8, 4>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    if (async_ok && N > 32 && ctas(64, 64) >= nsm)
+        return launch_exact_update_c<4, 4>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (short_ctas && N > 32 && ctas(128, 64) >= nsm)
         return launch_exact_update<8, 4, DESC, SKIP_ZERO>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (ctas(128, 128) >= nsm)
