@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
     const int h = (int)(a.n - a.j0);
     int rend = rbeg + a.rp;
     if (rend > h) rend = h;
+    const long long t_start = clock64();
     double r[R][PNB];
     int myrow[R];
 #pragma unroll
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     cl.sync();  // barriers initialised and every CTA running before the first push
+    const long long t_loaded = clock64();
     PanelLoop L;
     L.cs = cs;
     L.me = me;
@@ -491,11 +493,16 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
     if (nb > 6 * PKB) panel_cols<R, 6 * PKB>(r, myrow, sm, cl, L);
     if (nb > 7 * PKB) panel_cols<R, 7 * PKB>(r, myrow, sm, cl, L);
     cl.sync();  // no CTA may exit while others may still write its shared memory
+    const long long t_loop = clock64();
     if (me == 0 && tid == 0) {
         for (int k = 0; k < nb; ++k) a.piv[a.j0 + k] = a.j0 + sm.piv[k];
         if (L.info_col >= 0 && *a.info == 0) *a.info = (int32_t)(a.j0 + L.info_col + 1);
-        if (L.dbg_on)
+        if (L.dbg_on) {
             for (int k = 0; k < 8 * nb; ++k) a.dbg[k] = sm.dclk[k];
+            a.dbg[8 * nb + 0] = t_start;
+            a.dbg[8 * nb + 1] = t_loaded;
+            a.dbg[8 * nb + 2] = t_loop;
+        }
     }
 #pragma unroll
     for (int q = 0; q < R; ++q)
@@ -504,6 +511,7 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
             for (int j = 0; j < PNB; ++j)
                 if (j < nb) a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] = r[q][j];
     if (a.J1 > a.J0 && me == 0) panel_epilogue<R>(r, a, sm.piv);
+    if (a.dbg && me == 0 && tid == 0) a.dbg[8 * nb + 3] = clock64();
 }
 
 static int max_cluster() {

@@ -17,7 +17,7 @@ rng = np.random.default_rng(0)
 A0 = lm.DenseMatrix(rng.uniform(-1, 1, (n, n)) + n * np.eye(n))
 piv = torch.empty(n, dtype=torch.int64, device="cuda")
 info = torch.zeros(1, dtype=torch.int32, device="cuda")
-clk = torch.zeros(8 * 32, dtype=torch.int64, device="cuda")
+clk = torch.zeros(8 * 32 + 8, dtype=torch.int64, device="cuda")
 for rep in range(3):
     A = A0.data.t().contiguous().t()
     torch.cuda.synchronize()
@@ -27,7 +27,10 @@ for rep in range(3):
     e1.record()
     torch.cuda.synchronize()
     print("panel us", e0.elapsed_time(e1) * 1e3)
-c = clk.cpu().numpy().reshape(32, 8).astype(np.float64)
+allc = clk.cpu().numpy().astype(np.float64)
+c = allc[:256].reshape(32, 8)
+t = allc[256:260]
+print("kernel phases (cycles): load+cluster sync %.0f, column loop %.0f, write-back %.0f" % (t[1] - t[0], t[2] - t[1], t[3] - t[2]))
 names = ["wait", "winner", "swap+col", "argmax", "syncthr", "push+arrive", "rest upd", "->next"]
 d = np.stack([c[:, 1] - c[:, 0], c[:, 2] - c[:, 1], c[:, 3] - c[:, 2], c[:, 4] - c[:, 3], c[:, 5] - c[:, 4],
               c[:, 6] - c[:, 5], c[:, 7] - c[:, 6], np.r_[c[1:, 0] - c[:-1, 7], 0]], 1)
