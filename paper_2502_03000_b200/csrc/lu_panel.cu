@@ -71,7 +71,7 @@ __device__ __forceinline__ void panel_epilogue(const double (&r)[R][PNB], const 
         const int lane = tid;
         int top_src = lane, bkey = -1, bsrc = 0, nbot = 0;
         for (int k = 0; k < nb; ++k) {
-            const int p = (int)lpiv[k];
+            const int p = (int)(a.piv[a.j0 + k] - a.j0);  // (written by this CTA's thread 0)
             if (p == k) continue;
             const int a_src = __shfl_sync(0xffffffffu, top_src, k);
             int b_src;
@@ -504,13 +504,38 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
             a.dbg[8 * nb + 2] = t_loop;
         }
     }
+    // write-back through shared memory (the whole PanelSmem is dead now),
+    // 4 columns per pass, so each warp stores whole column segments with
+    // 16-byte lanes instead of 8-byte per-thread row stores
+    {
+        constexpr int WC = 4, LDW = R * PT + 2;
+        static_assert(sizeof(PanelSmem) >= sizeof(double) * WC * LDW, "write-back staging fits");
+        double *wb = reinterpret_cast<double *>(&sm);
+        const int nrows = rend - rbeg;
+        const bool vec = ((a.j0 + rbeg) % 2 == 0) && (a.lda % 2 == 0) && (((uintptr_t)a.A & 15) == 0);
+        __syncthreads();  // all shared-memory traffic of the column loop is over
 #pragma unroll
-    for (int q = 0; q < R; ++q)
-        if (myrow[q] >= 0)
+        for (int c0 = 0; c0 < PNB; c0 += WC) {
+            if (c0 >= nb) break;
 #pragma unroll
-            for (int j = 0; j < PNB; ++j)
-                if (j < nb) a.A[(a.j0 + myrow[q]) + (a.j0 + j) * a.lda] = r[q][j];
-    if (a.J1 > a.J0 && me == 0) panel_epilogue<R>(r, a, sm.piv);
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int j = 0; j < WC; ++j) wb[j * LDW + tid + q * PT] = r[q][c0 + j];
+            __syncthreads();
+            for (int j = 0; j < WC && c0 + j < nb; ++j) {
+                double *col = a.A + (a.j0 + rbeg) + (int64_t)(a.j0 + c0 + j) * a.lda;
+                if (vec) {
+                    for (int i = 2 * tid; i + 1 < nrows; i += 2 * PT)
+                        *reinterpret_cast<double2 *>(col + i) = make_double2(wb[j * LDW + i], wb[j * LDW + i + 1]);
+                    if ((nrows & 1) && tid == 0) col[nrows - 1] = wb[j * LDW + nrows - 1];
+                } else {
+                    for (int i = tid; i < nrows; i += PT) col[i] = wb[j * LDW + i];
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (a.J1 > a.J0 && me == 0) panel_epilogue<R>(r, a, nullptr);
     if (a.dbg && me == 0 && tid == 0) a.dbg[8 * nb + 3] = clock64();
 }
 
