@@ -41,6 +41,43 @@ def test_solve_batched_bitwise_vs_per_instance_reference(n, kind):
             assert bits_equal(x[i], ref)
 
 
+@pytest.mark.parametrize("n", [1, 2, 8, 9, 15, 16, 17, 24, 31, 32, 33, 40, 48, 50, 57, 63, 64])
+@pytest.mark.parametrize("with_lu", [False, True])
+def test_lu_solve_batched_entry_bitwise(n, with_lu):
+    """lm_lu_solve_batched (solve-only: the rolled shifted-row kernel; with
+    LU output: the unrolled kernel): x and pivots bit-identical to the
+    reference's _lu_factor + _lu_solve_inplace, general (pivoting) matrices
+    and ties (repeated magnitudes) included."""
+    from paper_2502_03000_b200 import _native as N
+
+    rng = np.random.default_rng(1000 + n)
+    bt = 29
+    A = rng.uniform(-1, 1, (bt, n, n))
+    A[1::4] = np.round(A[1::4] * 4) / 4          # many equal |values|: first-maximum tie rule
+    A[2::4] += n * np.eye(n)[None]
+    b = rng.uniform(-1, 1, (bt, n, 1))
+    At = stack_fortran(A)
+    x = torch.tensor(b[:, :, 0], device="cuda").contiguous()
+    piv = torch.zeros((bt, n), dtype=torch.int64, device="cuda")
+    info = torch.zeros(bt, dtype=torch.int32, device="cuda")
+    lu = torch.zeros((bt, n, n), dtype=torch.float64, device="cuda") if with_lu else None
+    N.call("lm_lu_solve_batched", 0, n, bt, At.data_ptr(), x.data_ptr(), lu.data_ptr() if with_lu else None,
+           piv.data_ptr(), info.data_ptr())
+    torch.cuda.synchronize()
+    xs, ps, inf = x.cpu().numpy(), piv.cpu().numpy(), info.cpu().numpy()
+    for i in range(bt):
+        rc, lur, pr = O.lu_factor(np.asfortranarray(A[i]))
+        assert inf[i] == rc, i
+        if rc:
+            continue
+        assert np.array_equal(ps[i], pr), i
+        xr = np.array(b[i], order="F")
+        O.lu_solve(lur, pr, xr)
+        assert bits_equal(xs[i], xr[:, 0]), i
+        if with_lu:
+            assert bits_equal(lu[i].cpu().numpy().reshape(n, n).T, lur), i
+
+
 def test_solve_batched_rule_logs_match_single_instance_planner():
     rng = np.random.default_rng(3)
     n, bt = 16, 5
