@@ -179,7 +179,9 @@ def test_triple_diag_dot():
 
 
 GEMM_SHAPES = [(1, 1, 1), (7, 5, 1), (1, 5, 7), (4096, 64, 1), (13, 17, 19), (64, 64, 64), (100, 8000, 100),
-               (8000, 100, 100), (130, 70, 90)]
+               (8000, 100, 100), (130, 70, 90),
+               # ragged edge tiles along one or both dimensions
+               (65, 300, 128), (128, 33, 2000), (3000, 40, 97), (120, 5000, 72)]
 
 
 @pytest.mark.parametrize("pqr", GEMM_SHAPES)
