@@ -19,6 +19,8 @@
 // Persistent CTAs loop over the instances of the class.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -416,6 +418,170 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_half(int64_t batch, co
     }
 }
 
+// n = 128 f64, "stream": ONE CTA of 16 warps per SM computes whole
+// instances (warp tile 32 x 32 of the 128 x 128 product, DMMA), and
+// overlaps each instance's main loop with the PREVIOUS instance's
+// epilogue: the previous product sits in a shared-memory buffer P and
+// every 8-row chunk of the main loop also finishes 1/16 of
+// E_prev = P + C % D (one 16-byte pair per thread, loads issued before the
+// chunk's DMMAs, so their latency hides behind them).  The cluster kernel
+// above alternates a DMMA phase and an HBM phase per instance (two CTAs
+// per SM that run in phase: 35k + 16k clocks per round, measured); here
+// the DMMA pipe and HBM are busy at the same time.  A 16-warp team is
+// needed to keep DMMA fed (one 8-warp team alone reaches half the pipe
+// rate, measured).  3-stage cp.async ring of 8-row chunks + P (130-double
+// columns) = 227 KB of shared memory.
+constexpr int SKC = 8, SST = 3, SLDK = SKC + 4, SLDP = HN + 2;
+struct alignas(128) SmemStream {
+    double a[SST][HN * SLDK];   // A(k, m): [m][k]
+    double b[SST][HN * SLDK];   // B(k, n): [n][k]
+    double ac[SST][SKC * SLDP]; // A(i, k): [k][i]
+    double p[HN * SLDP];        // previous instance's product: [n][m]
+    double red[16];
+};
+
+__device__ __forceinline__ void stage_stream(SmemStream &sm, int buf, const double *pa, const double *pb, int c,
+                                             int tid) {
+    // 512 threads, one 16-byte piece of each operand per thread
+    const int k0 = c * SKC;
+    {
+        const int col = tid >> 2, piece = tid & 3;
+        cpa16(&sm.a[buf][col * SLDK + piece * 2], pa + (int64_t)col * HN + k0 + piece * 2);
+        cpa16(&sm.b[buf][col * SLDK + piece * 2], pb + (int64_t)col * HN + k0 + piece * 2);
+    }
+    {
+        const int kl = tid >> 6, piece = tid & 63;
+        cpa16(&sm.ac[buf][kl * SLDP + piece * 2], pa + (int64_t)(k0 + kl) * HN + piece * 2);
+    }
+}
+
+__global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, const double *__restrict__ A,
+                                                                 const double *__restrict__ B,
+                                                                 const double *__restrict__ C,
+                                                                 const double *__restrict__ D, double *__restrict__ E,
+                                                                 double *__restrict__ S) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SmemStream &sm = *reinterpret_cast<SmemStream *>(smraw);
+    constexpr int NCH = HN / SKC;  // 16 chunks per instance
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
+    const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
+    // epilogue pair of this thread in chunk c: elements e, e+1 with e = 2*(c*512 + tid)
+    auto epi_off = [&](int c) -> int64_t {
+        const int e = 2 * (c * 512 + tid);
+        return (int64_t)e;  // column-major within the instance: n = e / 128, m = e % 128
+    };
+    auto p_off = [&](int c) -> int {
+        const int e = 2 * (c * 512 + tid), n = e >> 7, m = e & 127;
+        return n * SLDP + m;
+    };
+    // prologue: chunks 0 .. SST-2 of instance 0
+#pragma unroll
+    for (int c = 0; c < SST - 1; ++c) {
+        if (J > 0) stage_stream(sm, c, A + blockIdx.x * nn, B + blockIdx.x * nn, c, tid);
+        cpa_commit();
+    }
+    int gch = 0;  // global chunk counter (ring position)
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t b = blockIdx.x + j * G;
+        const double *pa = A + b * nn, *pb = B + b * nn;
+        const bool prev = j > 0;
+        const int64_t bp = b - G;  // previous instance (valid when prev)
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+        double tr = 0.0;
+        double2 cn_, dn_;  // C, D of the previous instance's pair for the next chunk
+        if (prev) {
+            cn_ = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(0)));
+            dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(0)));
+        }
+        for (int c = 0; c < NCH; ++c, ++gch) {
+            const int buf = gch % SST;
+            cpa_wait<SST - 2>();
+            __syncthreads();  // chunk visible; the buffer of chunk gch-1 is free
+            {
+                // refill the ring SST-1 chunks ahead (this instance, else the next)
+                const int cn = c + SST - 1;
+                const int nb = (gch + SST - 1) % SST;
+                if (cn < NCH)
+                    stage_stream(sm, nb, pa, pb, cn, tid);
+                else if (j + 1 < J)
+                    stage_stream(sm, nb, pa + G * nn, pb + G * nn, cn - NCH, tid);
+                cpa_commit();
+            }
+            double2 cv = cn_, dv = dn_;
+            if (prev && c + 1 < NCH) {
+                cn_ = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(c + 1)));
+                dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(c + 1)));
+            }
+            const double *as = sm.a[buf];
+            const double *bs = sm.b[buf];
+#pragma unroll
+            for (int kk = 0; kk < SKC; kk += 4) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * SLDK + kk + fc];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + fr) * SLDK + kk + fc];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) dmma884(acc[i][q], af[i], bf[q]);
+            }
+            {
+                // trace terms: sum_{k in chunk} sum_i A(i,k) B(k,i); 2 per thread
+                const double *ac = sm.ac[buf];
+                const int i = tid & 127, k2 = (tid >> 7) * 2;
+                tr = fma(ac[k2 * SLDP + i], bs[i * SLDK + k2], tr);
+                tr = fma(ac[(k2 + 1) * SLDP + i], bs[i * SLDK + k2 + 1], tr);
+            }
+            if (prev) {
+                const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[p_off(c)]);
+                double2 ev;
+                ev.x = radd(pv.x, rmul(cv.x, dv.x));
+                ev.y = radd(pv.y, rmul(cv.y, dv.y));
+                __stcs(reinterpret_cast<double2 *>(E + bp * nn + epi_off(c)), ev);
+            }
+        }
+        __syncthreads();  // every read of P (previous product) done
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) sm.p[(wn + q * 8 + 2 * fc + u) * SLDP + wm + i * 8 + fr] = acc[i][q][u];
+        // trace: fixed-order block sum
+        tr = warp_sum(tr);
+        if (lane == 0) sm.red[warp] = tr;
+        __syncthreads();
+        if (tid == 0) {
+            double t = sm.red[0];
+#pragma unroll
+            for (int q = 1; q < 16; ++q) t = radd(t, sm.red[q]);
+            S[b] = t;
+        }
+    }
+    if (J > 0) {
+        // drain: the last instance's epilogue
+        const int64_t bl = blockIdx.x + (J - 1) * G;
+#pragma unroll 4
+        for (int c = 0; c < NCH; ++c) {
+            const double2 cv = __ldcs(reinterpret_cast<const double2 *>(C + bl * nn + epi_off(c)));
+            const double2 dv = __ldcs(reinterpret_cast<const double2 *>(D + bl * nn + epi_off(c)));
+            const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[p_off(c)]);
+            double2 ev;
+            ev.x = radd(pv.x, rmul(cv.x, dv.x));
+            ev.y = radd(pv.y, rmul(cv.y, dv.y));
+            __stcs(reinterpret_cast<double2 *>(E + bl * nn + epi_off(c)), ev);
+        }
+    }
+}
+
 }  // namespace
 
 // Generic fallback (any n): one CTA per instance, SIMT, 32 x 32 tiles.
@@ -478,6 +644,22 @@ __global__ void __launch_bounds__(256) atb_schur_trace_generic(int64_t n, const 
     tacc = block_sum<T, 256>(tacc, red);
     if (threadIdx.x == 0) S[b] = tacc;
 }
+
+int launch_stream(int64_t batch, const double *a, const double *b, const double *c, const double *d, double *e,
+                  double *s, cudaStream_t st) {
+    auto kern = atb_schur_trace_stream;
+    const size_t smem = sizeof(SmemStream);
+    static int grid = 0;
+    if (!grid) {
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = resident_grid(kern, 512, smem);
+    }
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, 512, smem, st>>>(batch, a, b, c, d, e, s);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
 
 template <class T, int N>
 int launch_tc(int64_t batch, const T *a, const T *b, const T *c, const T *d, T *e, T *s, cudaStream_t st) {
@@ -544,6 +726,12 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
     if (aligned && n == 64) return launch_tc<T, 64>(batch, a, b, c, d, e, s, st);
     // n = 128: the two-CTA split wins for f64 (17.6 vs 19.7 ms on config 5a's
     // 87k instances); FP32 keeps the one-CTA kernel (10.0 vs 11.7 ms)
+    static const bool stream128 = [] {
+        const char *v = getenv("LM_5A_STREAM");  // 0: the two-CTA cluster kernel
+        return !(v && v[0] == '0');
+    }();
+    if constexpr (sizeof(T) == 8)
+        if (aligned && n == 128 && stream128) return launch_stream(batch, a, b, c, d, e, s, st);
     if (aligned && n == 128 && sizeof(T) == 8) return launch_half<T>(batch, a, b, c, d, e, s, st);
     if (aligned && n == 128) return launch_tc<T, 128>(batch, a, b, c, d, e, s, st);
     atb_schur_trace_generic<T><<<(unsigned)batch, 256, 0, st>>>(n, a, b, c, d, e, s);

@@ -1,0 +1,66 @@
+// dmma_occ_probe.cu -- DMMA (mma.sync.m8n8k4.f64) throughput versus resident
+// warps per SM, 16 independent accumulators per warp (the warp tile of the
+// GEMM / batched kernels), operands from registers or shared memory.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/dmma_occ_probe tools/dmma_occ_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+constexpr int ITERS = 2048;
+template <bool SMEM>
+__global__ void k(double *out, double a, double b) {
+    __shared__ double sa[32 * 20], sb[32 * 20];
+    for (int i = threadIdx.x; i < 32 * 20; i += blockDim.x) sa[i] = a + i, sb[i] = b - i;
+    __syncthreads();
+    double c[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+    const int lane = threadIdx.x & 31, fr = lane >> 2, fc = lane & 3;
+    double av = a + threadIdx.x, bv = b - threadIdx.x;
+    for (int it = 0; it < ITERS; ++it) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            af[i] = SMEM ? sa[(i * 8 + fr) * 20 + (it & 3) * 4 + fc] : av + i;
+            bf[i] = SMEM ? sb[(i * 8 + fr) * 20 + (it & 3) * 4 + fc] : bv - i;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(c[i][j][0]), "+d"(c[i][j][1])
+                             : "d"(af[i]), "d"(bf[j]));
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s += c[i][j][0] + c[i][j][1];
+    if (s == 1.2345) out[0] = s;
+}
+int main() {
+    int nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    double *d;
+    cudaMalloc(&d, 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int smem = 0; smem < 2; ++smem)
+        for (int wps : {4, 8, 12, 16, 24, 32}) {
+            // one CTA per SM with wps warps
+            auto kern = smem ? k<true> : k<false>;
+            kern<<<nsm, wps * 32>>>(d, 1.0000001, 1e-9);
+            cudaDeviceSynchronize();
+            cudaEventRecord(e0);
+            kern<<<nsm, wps * 32>>>(d, 1.0000001, 1e-9);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double flops = 2.0 * 256 * 16 * (double)ITERS * wps * nsm;
+            printf("%s warps/SM %2d: %.2f TFLOP/s\n", smem ? "smem" : "regs", wps, flops / ms / 1e9);
+        }
+    return cudaGetLastError() != cudaSuccess;
+}
