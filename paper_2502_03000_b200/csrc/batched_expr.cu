@@ -438,22 +438,37 @@ struct alignas(128) SmemStream {
     double ac[SST][SKC * SLDP]; // A(i, k): [k][i]
     double p[HN * SLDP];        // previous instance's product: [n][m]
     double red[16];
+    unsigned long long full[SST], empty[SST];  // ring mbarriers
 };
 
-__device__ __forceinline__ void stage_stream(SmemStream &sm, int buf, const double *pa, const double *pb, int c,
-                                             int tid) {
-    // 512 threads, one 16-byte piece of each operand per thread
+__device__ __forceinline__ unsigned sm_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            sm_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// one warp's copy of a whole chunk (48 x 16 B per lane) into stage `buf`;
+// completion arrives on full[buf] (expected count 32)
+__device__ __forceinline__ void produce_chunk(SmemStream &sm, int buf, const double *pa, const double *pb, int c,
+                                              int lane) {
     const int k0 = c * SKC;
-    {
-        const int col = tid >> 2, piece = tid & 3;
+#pragma unroll 4
+    for (int e = lane; e < HN * 4; e += 32) {
+        const int col = e >> 2, piece = e & 3;
         cpa16(&sm.a[buf][col * SLDK + piece * 2], pa + (int64_t)col * HN + k0 + piece * 2);
         cpa16(&sm.b[buf][col * SLDK + piece * 2], pb + (int64_t)col * HN + k0 + piece * 2);
     }
-    {
-        const int kl = tid >> 6, piece = tid & 63;
+#pragma unroll 4
+    for (int e = lane; e < SKC * 64; e += 32) {
+        const int kl = e >> 6, piece = e & 63;
         cpa16(&sm.ac[buf][kl * SLDP + piece * 2], pa + (int64_t)(k0 + kl) * HN + piece * 2);
     }
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sm_addr(&sm.full[buf])) : "memory");
 }
+
 
 __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, const double *__restrict__ A,
                                                                  const double *__restrict__ B,
@@ -477,13 +492,31 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, 
         const int e = 2 * (c * 512 + tid), n = e >> 7, m = e & 127;
         return n * SLDP + m;
     };
-    // prologue: chunks 0 .. SST-2 of instance 0
+    if (tid == 0) {
 #pragma unroll
-    for (int c = 0; c < SST - 1; ++c) {
-        if (J > 0) stage_stream(sm, c, A + blockIdx.x * nn, B + blockIdx.x * nn, c, tid);
-        cpa_commit();
+        for (int q = 0; q < SST; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.full[q])), "r"(32));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.empty[q])), "r"(16));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    int gch = 0;  // global chunk counter (ring position)
+    __syncthreads();
+    // Ring without CTA-wide barriers: chunk g + SST - 1 is copied by warp
+    // g % 16 (a rotating producer) once every warp has released chunk g - 1
+    // (empty mbarrier); consumers wait only for their chunk's data (full
+    // mbarrier).  A barrier per chunk would line all warps up on the DMMA
+    // latency (tools/dmma_occ_probe.cu: a __syncthreads per 32 DMMAs per warp
+    // costs ~25% of the pipe).
+    const int64_t total = J * NCH;
+    auto produce = [&](int64_t gp) {
+        const int s = (int)(gp % SST);
+        const int64_t u = gp / SST;
+        if (u > 0) mbar_wait(&sm.empty[s], (unsigned)((u - 1) & 1));
+        const int64_t bi = blockIdx.x + (gp / NCH) * G;
+        produce_chunk(sm, s, A + bi * nn, B + bi * nn, (int)(gp % NCH), lane);
+    };
+    if (warp < SST - 1 && warp < total) produce(warp);
+    int64_t gch = 0;  // global chunk counter (ring position)
     for (int64_t j = 0; j < J; ++j) {
         const int64_t b = blockIdx.x + j * G;
         const double *pa = A + b * nn, *pb = B + b * nn;
@@ -501,24 +534,14 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, 
             dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(0)));
         }
         for (int c = 0; c < NCH; ++c, ++gch) {
-            const int buf = gch % SST;
-            cpa_wait<SST - 2>();
-            __syncthreads();  // chunk visible; the buffer of chunk gch-1 is free
-            {
-                // refill the ring SST-1 chunks ahead (this instance, else the next)
-                const int cn = c + SST - 1;
-                const int nb = (gch + SST - 1) % SST;
-                if (cn < NCH)
-                    stage_stream(sm, nb, pa, pb, cn, tid);
-                else if (j + 1 < J)
-                    stage_stream(sm, nb, pa + G * nn, pb + G * nn, cn - NCH, tid);
-                cpa_commit();
-            }
+            const int buf = (int)(gch % SST);
+            if (warp == (int)(gch % 16) && gch + SST - 1 < total) produce(gch + SST - 1);
             double2 cv = cn_, dv = dn_;
             if (prev && c + 1 < NCH) {
                 cn_ = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(c + 1)));
                 dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(c + 1)));
             }
+            mbar_wait(&sm.full[buf], (unsigned)((gch / SST) & 1));
             const double *as = sm.a[buf];
             const double *bs = sm.b[buf];
 #pragma unroll
@@ -540,6 +563,8 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, 
                 tr = fma(ac[k2 * SLDP + i], bs[i * SLDK + k2], tr);
                 tr = fma(ac[(k2 + 1) * SLDP + i], bs[i * SLDK + k2 + 1], tr);
             }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.empty[buf])) : "memory");
             if (prev) {
                 const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[p_off(c)]);
                 double2 ev;

@@ -6,7 +6,7 @@
 #include <cuda_runtime.h>
 constexpr int ITERS = 2048;
 template <bool SMEM>
-__global__ void k(double *out, double a, double b) {
+__global__ void k(double *out, double a, double b, int sync_every) {
     __shared__ double sa[32 * 20], sb[32 * 20];
     for (int i = threadIdx.x; i < 32 * 20; i += blockDim.x) sa[i] = a + i, sb[i] = b - i;
     __syncthreads();
@@ -31,6 +31,7 @@ __global__ void k(double *out, double a, double b) {
                 asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                              : "+d"(c[i][j][0]), "+d"(c[i][j][1])
                              : "d"(af[i]), "d"(bf[j]));
+        if (sync_every && (it % sync_every) == sync_every - 1) __syncthreads();
     }
     double s = 0;
 #pragma unroll
@@ -47,20 +48,21 @@ int main() {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int smem = 0; smem < 2; ++smem)
-        for (int wps : {4, 8, 12, 16, 24, 32}) {
+    for (int se : {0, 1, 2, 4})
+    for (int smem = 1; smem < 2; ++smem)
+        for (int wps : {8, 16}) {
             // one CTA per SM with wps warps
             auto kern = smem ? k<true> : k<false>;
-            kern<<<nsm, wps * 32>>>(d, 1.0000001, 1e-9);
+            kern<<<nsm, wps * 32>>>(d, 1.0000001, 1e-9, se);
             cudaDeviceSynchronize();
             cudaEventRecord(e0);
-            kern<<<nsm, wps * 32>>>(d, 1.0000001, 1e-9);
+            kern<<<nsm, wps * 32>>>(d, 1.0000001, 1e-9, se);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms = 0;
             cudaEventElapsedTime(&ms, e0, e1);
             const double flops = 2.0 * 256 * 16 * (double)ITERS * wps * nsm;
-            printf("%s warps/SM %2d: %.2f TFLOP/s\n", smem ? "smem" : "regs", wps, flops / ms / 1e9);
+            printf("%s warps/SM %2d sync every %d x 16 DMMA: %.2f TFLOP/s\n", smem ? "smem" : "regs", wps, se, flops / ms / 1e9);
         }
     return cudaGetLastError() != cudaSuccess;
 }
