@@ -454,21 +454,23 @@ __device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned pari
 // completion arrives on full[buf] (expected count 32)
 __device__ __forceinline__ void produce_chunk(SmemStream &sm, int buf, const double *pa, const double *pb, int c,
                                               int lane) {
+    // every offset is affine in the unrolled index: three base pointers per
+    // lane, immediate offsets for the 48 copies
     const int k0 = c * SKC;
-#pragma unroll 4
-    for (int e = lane; e < HN * 4; e += 32) {
-        const int col = e >> 2, piece = e & 3;
-        cpa16(&sm.a[buf][col * SLDK + piece * 2], pa + (int64_t)col * HN + k0 + piece * 2);
-        cpa16(&sm.b[buf][col * SLDK + piece * 2], pb + (int64_t)col * HN + k0 + piece * 2);
+    const int col = lane >> 2, piece = lane & 3;
+    double *sa = &sm.a[buf][col * SLDK + piece * 2], *sb = &sm.b[buf][col * SLDK + piece * 2];
+    const double *ga = pa + (int64_t)col * HN + k0 + piece * 2, *gb = pb + (int64_t)col * HN + k0 + piece * 2;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        cpa16(sa + r * 8 * SLDK, ga + r * 8 * HN);
+        cpa16(sb + r * 8 * SLDK, gb + r * 8 * HN);
     }
-#pragma unroll 4
-    for (int e = lane; e < SKC * 64; e += 32) {
-        const int kl = e >> 6, piece = e & 63;
-        cpa16(&sm.ac[buf][kl * SLDP + piece * 2], pa + (int64_t)(k0 + kl) * HN + piece * 2);
-    }
+    double *sc = &sm.ac[buf][lane * 2];
+    const double *gc = pa + (int64_t)k0 * HN + lane * 2;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cpa16(sc + (r >> 1) * SLDP + (r & 1) * 64, gc + (r >> 1) * HN + (r & 1) * 64);
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sm_addr(&sm.full[buf])) : "memory");
 }
-
 
 __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, const double *__restrict__ A,
                                                                  const double *__restrict__ B,
@@ -517,8 +519,17 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, 
     };
     if (warp < SST - 1 && warp < total) produce(warp);
     int64_t gch = 0;  // global chunk counter (ring position)
+    int64_t b_cur = 0;
+    auto epi = [&](int c, double2 cv, double2 dv) {
+        const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[p_off(c)]);
+        double2 ev;
+        ev.x = radd(pv.x, rmul(cv.x, dv.x));
+        ev.y = radd(pv.y, rmul(cv.y, dv.y));
+        __stcs(reinterpret_cast<double2 *>(E + (b_cur - G) * nn + epi_off(c)), ev);
+    };
     for (int64_t j = 0; j < J; ++j) {
         const int64_t b = blockIdx.x + j * G;
+        b_cur = b;
         const double *pa = A + b * nn, *pb = B + b * nn;
         const bool prev = j > 0;
         const int64_t bp = b - G;  // previous instance (valid when prev)
@@ -565,13 +576,7 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, 
             }
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.empty[buf])) : "memory");
-            if (prev) {
-                const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[p_off(c)]);
-                double2 ev;
-                ev.x = radd(pv.x, rmul(cv.x, dv.x));
-                ev.y = radd(pv.y, rmul(cv.y, dv.y));
-                __stcs(reinterpret_cast<double2 *>(E + bp * nn + epi_off(c)), ev);
-            }
+            if (prev) epi(c, cv, dv);
         }
         __syncthreads();  // every read of P (previous product) done
 #pragma unroll
