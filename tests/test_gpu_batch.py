@@ -122,6 +122,33 @@ def test_atb_schur_trace_vs_oracle(n, dtype):
         assert abs(s[i] - tr) <= tol * max(abs(tr), np.sum(np.abs(A * B.T)) * 1e-2)
 
 
+@pytest.mark.parametrize("n", [32, 64, 128])
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_atb_schur_trace_many_instances_per_cta(n, dtype):
+    """Batches larger than the persistent grid: every CTA runs several
+    instances, so the n = 128 kernel's overlapped epilogue (instance j's E
+    finished during instance j+1's main loop) and its drain are exercised;
+    sampled instances against the oracle."""
+    rng = np.random.default_rng(7 * n)
+    bt = 700
+    ops = [rng.uniform(-1, 1, (bt, n, n)) for _ in range(4)]
+    if dtype == torch.float32:
+        ops = [o.astype(np.float32).astype(np.float64) for o in ops]
+    E, s = atb_schur_trace(*(stack_fortran(o, dtype=dtype) for o in ops))
+    E, s = E.cpu().numpy(), s.cpu().numpy()
+    pops, pargs, *_ = parse_program("x0 x1 x2 * +")
+    tol = 1e-12 if dtype == torch.float64 else 1e-5
+    for i in sorted({0, 1, 147, 148, 149, 295, 296, 297, 443, 444, 591, 592, 699, int(rng.integers(0, bt))}):
+        A, B, C, D = (np.asfortranarray(o[i]) for o in ops)
+        g = np.zeros((n, n), order="F")
+        O.gemm(A.T, B, g)
+        Er = np.zeros((n, n), order="F")
+        O.program(pops.numpy(), pargs.numpy(), [], [g, C, D], Er)
+        assert np.max(np.abs(E[i] - Er)) <= tol * max(np.max(np.abs(Er)), 1e-30), i
+        tr = O.trace_of_product(A, B)
+        assert abs(s[i] - tr) <= tol * max(abs(tr), np.sum(np.abs(A * B.T)) * 1e-2), i
+
+
 @pytest.mark.parametrize("n", [1, 3, 5, 16, 33, 64])
 def test_classified_kernel_matches_structure_scan(n):
     """The one-pass classify+solve kernel assigns every instance the class
