@@ -612,6 +612,211 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, 
     }
 }
 
+// n = 128 f32: the same streaming structure with A.T @ B on the TENSOR
+// cores in 3xTF32: every operand x is split into x_hi = tf32(x) and
+// x_lo = tf32(x - x_hi), and a.b is accumulated as a_hi b_lo + a_lo b_hi +
+// a_hi b_hi (the dropped a_lo b_lo term is ~2^-22 of the product) in f32,
+// so results sit at FFMA accuracy (north star: 1e-5) while the products run
+// on mma.sync.m16n8k8.tf32 (275 TF/s measured on B200 vs 72 TF/s FFMA,
+// tools/tf32_probe.cu).  Warp tile 32 x 32 = 2 x 4 m16n8 tiles.  The trace
+// and the epilogue (E = round(P) + round(C*D)) stay scalar f32.
+constexpr int FKC = 16, FST = 4, FLDK = FKC + 4, FLDP = HN + 4;
+struct alignas(128) SmemStreamF {
+    float a[FST][HN * FLDK];    // A(k, m): [m][k]
+    float b[FST][HN * FLDK];    // B(k, n): [n][k]
+    float ac[FST][FKC * FLDP];  // A(i, k): [k][i]
+    float p[HN * FLDP];         // previous instance's product: [n][m]
+    float red[16];
+    unsigned long long full[FST], empty[FST];
+};
+
+__device__ __forceinline__ void produce_chunk_f(SmemStreamF &sm, int buf, const float *pa, const float *pb, int c,
+                                                int lane) {
+    const int k0 = c * FKC;
+    const int col = lane >> 2, piece = lane & 3;
+    float *sa = &sm.a[buf][col * FLDK + piece * 4], *sb = &sm.b[buf][col * FLDK + piece * 4];
+    const float *ga = pa + (int64_t)col * HN + k0 + piece * 4, *gb = pb + (int64_t)col * HN + k0 + piece * 4;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+        cpa16(sa + r * 8 * FLDK, ga + r * 8 * HN);
+        cpa16(sb + r * 8 * FLDK, gb + r * 8 * HN);
+    }
+    float *sc = &sm.ac[buf][lane * 4];
+    const float *gc = pa + (int64_t)k0 * HN + lane * 4;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cpa16(sc + r * FLDP, gc + r * HN);
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sm_addr(&sm.full[buf])) : "memory");
+}
+
+__device__ __forceinline__ void tf32_split(float x, unsigned &hi, unsigned &lo) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi) : "f"(x));
+    const float r = x - __uint_as_float(hi);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo) : "f"(r));
+}
+
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const unsigned (&a)[4], const unsigned (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_f32(int64_t batch, const float *__restrict__ A,
+                                                                     const float *__restrict__ B,
+                                                                     const float *__restrict__ C,
+                                                                     const float *__restrict__ D, float *__restrict__ E,
+                                                                     float *__restrict__ S) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SmemStreamF &sm = *reinterpret_cast<SmemStreamF *>(smraw);
+    constexpr int NCH = HN / FKC;  // 8 chunks per instance
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
+    const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
+    // epilogue vector of this thread in chunk c: elements 4v .. 4v+3, v = c*512 + tid
+    auto epi_off = [&](int c) -> int64_t { return (int64_t)4 * (c * 512 + tid); };
+    auto p_off = [&](int c) -> int {
+        const int e = 4 * (c * 512 + tid);
+        return (e >> 7) * FLDP + (e & 127);
+    };
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < FST; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.full[q])), "r"(32));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.empty[q])), "r"(16));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t total = J * NCH;
+    auto produce = [&](int64_t gp) {
+        const int s = (int)(gp % FST);
+        const int64_t u = gp / FST;
+        if (u > 0) mbar_wait(&sm.empty[s], (unsigned)((u - 1) & 1));
+        const int64_t bi = blockIdx.x + (gp / NCH) * G;
+        produce_chunk_f(sm, s, A + bi * nn, B + bi * nn, (int)(gp % NCH), lane);
+    };
+    // chunk g + FAHEAD is copied (into the stage of chunk g + FAHEAD - FST)
+    // while chunk g is consumed: FAHEAD chunks of copy latency cover and
+    // FST - FAHEAD chunks of slack before the stage must be free
+    constexpr int FAHEAD = FST - 2;
+#pragma unroll
+    for (int q = 0; q < FAHEAD; ++q)
+        if (warp == q && q < total) produce(q);
+    auto epi = [&](int64_t inst, int c, float4 cv, float4 dv) {
+        const float4 pv = *reinterpret_cast<const float4 *>(&sm.p[p_off(c)]);
+        float4 ev;
+        ev.x = radd(pv.x, rmul(cv.x, dv.x));
+        ev.y = radd(pv.y, rmul(cv.y, dv.y));
+        ev.z = radd(pv.z, rmul(cv.z, dv.z));
+        ev.w = radd(pv.w, rmul(cv.w, dv.w));
+        __stcs(reinterpret_cast<float4 *>(E + inst * nn + epi_off(c)), ev);
+    };
+    int64_t gch = 0;
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t b = blockIdx.x + j * G;
+        const bool prev = j > 0;
+        const int64_t bp = b - G;
+        float acc[2][4][4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) acc[i][q][u] = 0.f;
+        float tr = 0.f;
+        float4 cn_, dn_;
+        if (prev) {
+            cn_ = __ldcs(reinterpret_cast<const float4 *>(C + bp * nn + epi_off(0)));
+            dn_ = __ldcs(reinterpret_cast<const float4 *>(D + bp * nn + epi_off(0)));
+        }
+        for (int c = 0; c < NCH; ++c, ++gch) {
+            const int buf = (int)(gch % FST);
+            if (warp == (int)(gch % 16) && gch + FAHEAD < total) produce(gch + FAHEAD);
+            const float4 cv = cn_, dv = dn_;
+            if (prev && c + 1 < NCH) {
+                cn_ = __ldcs(reinterpret_cast<const float4 *>(C + bp * nn + epi_off(c + 1)));
+                dn_ = __ldcs(reinterpret_cast<const float4 *>(D + bp * nn + epi_off(c + 1)));
+            }
+            mbar_wait(&sm.full[buf], (unsigned)((gch / FST) & 1));
+            const float *as = sm.a[buf];
+            const float *bs = sm.b[buf];
+#pragma unroll
+            for (int kk = 0; kk < FKC; kk += 8) {
+                unsigned ah[2][4], al[2][4], bh[4][2], bl[4][2];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const float *ap = as + (wm + 16 * i + g8) * FLDK + kk + t4;
+                    tf32_split(ap[0], ah[i][0], al[i][0]);
+                    tf32_split(ap[8 * FLDK], ah[i][1], al[i][1]);
+                    tf32_split(ap[4], ah[i][2], al[i][2]);
+                    tf32_split(ap[8 * FLDK + 4], ah[i][3], al[i][3]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float *bp_ = bs + (wn + 8 * q + g8) * FLDK + kk + t4;
+                    tf32_split(bp_[0], bh[q][0], bl[q][0]);
+                    tf32_split(bp_[4], bh[q][1], bl[q][1]);
+                }
+                // three passes over the 8 tiles: 8 independent MMAs between
+                // two that accumulate into the same tile
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) mma_tf32(acc[i][q], ah[i], bl[q]);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) mma_tf32(acc[i][q], al[i], bh[q]);
+#pragma unroll
+                for (int i = 0; i < 2; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) mma_tf32(acc[i][q], ah[i], bh[q]);
+            }
+            {
+                // trace terms: 4 per thread
+                const float *ac = sm.ac[buf];
+                const int i = tid & 127, k4 = (tid >> 7) * 4;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tr = fmaf(ac[(k4 + q) * FLDP + i], bs[i * FLDK + k4 + q], tr);
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.empty[buf])) : "memory");
+            if (prev) epi(bp, c, cv, dv);
+        }
+        __syncthreads();  // every read of P done
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int m0 = wm + 16 * i + g8, n0 = wn + 8 * q + 2 * t4;
+                sm.p[n0 * FLDP + m0] = acc[i][q][0];
+                sm.p[(n0 + 1) * FLDP + m0] = acc[i][q][1];
+                sm.p[n0 * FLDP + m0 + 8] = acc[i][q][2];
+                sm.p[(n0 + 1) * FLDP + m0 + 8] = acc[i][q][3];
+            }
+        tr = warp_sum(tr);
+        if (lane == 0) sm.red[warp] = tr;
+        __syncthreads();
+        if (tid == 0) {
+            float t = sm.red[0];
+#pragma unroll
+            for (int q = 1; q < 16; ++q) t = radd(t, sm.red[q]);
+            S[b] = t;
+        }
+    }
+    if (J > 0) {
+        const int64_t bl = blockIdx.x + (J - 1) * G;
+#pragma unroll 2
+        for (int c = 0; c < NCH; ++c) {
+            const float4 cv = __ldcs(reinterpret_cast<const float4 *>(C + bl * nn + epi_off(c)));
+            const float4 dv = __ldcs(reinterpret_cast<const float4 *>(D + bl * nn + epi_off(c)));
+            epi(bl, c, cv, dv);
+        }
+    }
+}
+
 }  // namespace
 
 // Generic fallback (any n): one CTA per instance, SIMT, 32 x 32 tiles.
@@ -673,6 +878,21 @@ __global__ void __launch_bounds__(256) atb_schur_trace_generic(int64_t n, const 
         }
     tacc = block_sum<T, 256>(tacc, red);
     if (threadIdx.x == 0) S[b] = tacc;
+}
+
+int launch_stream_f32(int64_t batch, const float *a, const float *b, const float *c, const float *d, float *e,
+                      float *s, cudaStream_t st) {
+    auto kern = atb_schur_trace_stream_f32;
+    const size_t smem = sizeof(SmemStreamF);
+    static int grid = 0;
+    if (!grid) {
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = resident_grid(kern, 512, smem);
+    }
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, 512, smem, st>>>(batch, a, b, c, d, e, s);
+    LM_LAUNCHED(1);
+    return 0;
 }
 
 int launch_stream(int64_t batch, const double *a, const double *b, const double *c, const double *d, double *e,
@@ -760,8 +980,15 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
         const char *v = getenv("LM_5A_STREAM");  // 0: the two-CTA cluster kernel
         return !(v && v[0] == '0');
     }();
-    if constexpr (sizeof(T) == 8)
+    if constexpr (sizeof(T) == 8) {
         if (aligned && n == 128 && stream128) return launch_stream(batch, a, b, c, d, e, s, st);
+    } else {
+        static const bool tf32x3 = [] {
+            const char *v = getenv("LM_5A_TF32");  // 0: the FFMA kernel
+            return !(v && v[0] == '0');
+        }();
+        if (aligned && n == 128 && tf32x3) return launch_stream_f32(batch, a, b, c, d, e, s, st);
+    }
     if (aligned && n == 128 && sizeof(T) == 8) return launch_half<T>(batch, a, b, c, d, e, s, st);
     if (aligned && n == 128) return launch_tc<T, 128>(batch, a, b, c, d, e, s, st);
     atb_schur_trace_generic<T><<<(unsigned)batch, 256, 0, st>>>(n, a, b, c, d, e, s);
