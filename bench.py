@@ -284,8 +284,14 @@ class Config1(Workload):
         O.program(ops.numpy(), args.numpy(), [2.0, 1.0], [h["A"], h["B"], h["C"]], out)
 
 
-def _fp32_peak():
-    return 2.0 * _fp64_peak()[0]  # B200: FP32 FFMA issue rate is 2x FP64 (nominal)
+# The f32 n=128 batched kernel runs A.T*B as 3xTF32 on mma.sync.m16n8k8.tf32:
+# 275.2 TF/s measured (tools/tf32_probe.cu, profiles/r01_tf32_probe.txt),
+# three MMAs per product -> an effective f32 ceiling of a third of that.
+TF32_MMA_TFLOPS = 275.2
+
+
+def _tf32x3_peak():
+    return TF32_MMA_TFLOPS / 3.0, "3xTF32 effective (legacy mma.sync tf32 275.2 TF/s measured / 3)"
 
 
 def _fp64_peak():
@@ -947,7 +953,7 @@ def run_ours(args, wl, ws, rank, local):
             peak, peak_kind = _peaks()
             achieved, unit = work / (kms * 1e-3) / 1e9, "GB/s"
             if kflops is not None:
-                fpeak, fkind = _fp64_peak() if wl.dtype == "f64" else (_fp32_peak(), "nominal FP32 FFMA")
+                fpeak, fkind = _fp64_peak() if wl.dtype == "f64" else _tf32x3_peak()
                 if getattr(wl, "exact_fp64", False):
                     fpeak, fkind = fpeak / 2, fkind + "; /2 for exact mul+sub (no FMA)"
                 fach = kflops / (kms * 1e-3) / 1e12
@@ -964,7 +970,8 @@ def run_ours(args, wl, ws, rank, local):
                                 **({"TFLOP/s": f / (t * 1e-3) / 1e12} if f is not None else {}))
                         for n, w, t, f in kern}}
         if unit == "TFLOP/s":
-            roof["note"] = "FP64 (DMMA/DFMA) ceiling; sm_100a has no tcgen05 f64 kind"
+            roof["note"] = ("FP64 (DMMA/DFMA) ceiling; sm_100a has no tcgen05 f64 kind" if wl.dtype == "f64" else
+                            "f32 products on TF32 tensor cores (3xTF32, FFMA-level accuracy)")
 
     strong = getattr(wl, "scaling", "weak") == "strong"
     total_work = wl.work_per_step() * (1 if strong else ws)
