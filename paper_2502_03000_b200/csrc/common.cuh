@@ -47,6 +47,37 @@ void ensure_pool();
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// A kernel launched with launch_pdl() may start while the previous kernel in
+// the stream is still draining; it MUST call pdl_wait() before reading
+// anything that kernel wrote (griddepcontrol.wait returns once the
+// prerequisite grid has completed and its memory is visible).  A primary
+// kernel calls pdl_trigger() once its remaining work no longer needs the
+// SMs to itself, letting the dependent grid's CTAs launch early.  Chains of
+// short dependent kernels (GEMV + ordered finish, x3 in config 3a) lose
+// their launch gaps this way.  LM_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    if (!pdl_enabled()) {
+        kern<<<grid, block, smem, s>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Stream-ordered scratch (cudaMallocAsync); freed on the same stream.
 struct Scratch {
     void *p = nullptr;

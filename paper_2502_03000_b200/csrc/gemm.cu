@@ -110,6 +110,8 @@ __global__ void __launch_bounds__(kGv32Warps * 32, MINB) gemv_cm32(const T *__re
     const int64_t rb = blockIdx.x, c = blockIdx.y;
     const int64_t r0 = rb * RB + lane * RPT;
     const int64_t k0 = c * kGv32KC + w;
+    pdl_wait();  // M and x may be the previous kernel's output
+    pdl_trigger();
     T acc[RPT];
 #pragma unroll
     for (int l = 0; l < RPT; ++l) acc[l] = T(0);
@@ -170,6 +172,8 @@ __global__ void __launch_bounds__(256) gemv_finish(const T *__restrict__ part, i
     __shared__ T red[8][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    pdl_wait();
+    pdl_trigger();
     T acc = T(0);
     if (i < p) {
 #pragma unroll 4
@@ -203,8 +207,10 @@ template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_v
         Scratch part;
         if (int rc = part.alloc(sizeof(T) * p * chunks, s)) return rc;
         const dim3 grid((unsigned)rowblocks, (unsigned)chunks);
-        gemv_cm32<T, KCv, sizeof(T) == 8 ? 4 : 3><<<grid, kGv32Warps * 32, 0, s>>>((const T *)mv.ptr, ld, p, q, x, part.as<T>());
-        gemv_finish<T><<<(unsigned)ceil_div(p, 32), 256, 0, s>>>(part.as<T>(), p, chunks, to_vec<T>(yv));
+        LM_CUDA(launch_pdl(gemv_cm32<T, KCv, sizeof(T) == 8 ? 4 : 3>, grid, dim3(kGv32Warps * 32), 0, s,
+                           (const T *)mv.ptr, ld, p, q, x, part.as<T>()));
+        LM_CUDA(launch_pdl(gemv_finish<T>, dim3((unsigned)ceil_div(p, 32)), dim3(256), 0, s, (const T *)part.as<T>(), p,
+                           chunks, to_vec<T>(yv)));
         LM_LAUNCHED(2);
         return 0;
     }
@@ -381,6 +387,8 @@ template <bool CONTIG_OUTER, int BKT> constexpr int stage_doubles() {
 // accumulators), ST-stage cp.async ring with one barrier per K step.
 template <bool A_CM, bool B_CN, bool VA, bool VB, int BKT, int ST>
 __global__ void __launch_bounds__(kGmThreads) dgemm_dmma(GemmArgs g) {
+    pdl_wait();  // inputs may be the previous kernel's output (PDL)
+    pdl_trigger();
     extern __shared__ __align__(16) double gsm[];
     constexpr int SA = stage_doubles<A_CM, BKT>(), SB = stage_doubles<B_CN, BKT>();
     double *sA = gsm;
@@ -490,6 +498,8 @@ __global__ void __launch_bounds__(kGmThreads) dgemm_dmma(GemmArgs g) {
 // Few partials: one thread per element, loads unrolled (independent).
 __global__ void __launch_bounds__(256) splitk_finish_flat(const double *__restrict__ part, int64_t M, int64_t N,
                                                           int64_t nz, double *c, int64_t c_sm, int64_t c_sn, int syrk) {
+    pdl_wait();  // inputs may be the previous kernel's output (PDL)
+    pdl_trigger();
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t MN = M * N;
     if (e >= MN) return;
@@ -507,6 +517,8 @@ __global__ void __launch_bounds__(256) splitk_finish_flat(const double *__restri
 // sums are combined in warp order: a fixed tree, reproducible run to run.
 __global__ void __launch_bounds__(256) splitk_finish(const double *__restrict__ part, int64_t M, int64_t N, int64_t nz,
                                                      double *c, int64_t c_sm, int64_t c_sn, int syrk) {
+    pdl_wait();  // inputs may be the previous kernel's output (PDL)
+    pdl_trigger();
     __shared__ double red[8][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t e = (int64_t)blockIdx.x * 32 + lane;
@@ -537,7 +549,7 @@ int launch_dgemm_kernel(const GemmArgs &g, dim3 grid, cudaStream_t s) {
         LM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr = true;
     }
-    k<<<grid, kGmThreads, smem, s>>>(g);
+    LM_CUDA(launch_pdl(k, grid, dim3(kGmThreads), smem, s, g));
     LM_LAUNCHED(1);
     return 0;
 }
@@ -619,11 +631,11 @@ int dgemm_cfg(GemmArgs &g, bool a_cm, bool b_cn, bool va, bool vb, cudaStream_t 
     if (rc) return rc;
     if (splits > 1) {
         if (splits <= 16)
-            splitk_finish_flat<<<(unsigned)ceil_div(M * N, 256), 256, 0, s>>>(g.part, M, N, splits, g.c, g.c_sm,
-                                                                              g.c_sn, g.syrk);
+            LM_CUDA(launch_pdl(splitk_finish_flat, dim3((unsigned)ceil_div(M * N, 256)), dim3(256), 0, s,
+                               (const double *)g.part, M, N, (int64_t)splits, g.c, g.c_sm, g.c_sn, g.syrk));
         else
-            splitk_finish<<<(unsigned)ceil_div(M * N, 32), 256, 0, s>>>(g.part, M, N, splits, g.c, g.c_sm, g.c_sn,
-                                                                         g.syrk);
+            LM_CUDA(launch_pdl(splitk_finish, dim3((unsigned)ceil_div(M * N, 32)), dim3(256), 0, s,
+                               (const double *)g.part, M, N, (int64_t)splits, g.c, g.c_sm, g.c_sn, g.syrk));
         LM_LAUNCHED(1);
     }
     return 0;

@@ -89,6 +89,8 @@ template <class T, bool RIGHT>
 __global__ void __launch_bounds__(256) diag_scale_cols32(Vec<const T> d, const T *__restrict__ b, int64_t ldb,
                                                          T *__restrict__ out, int64_t ldo, int64_t rows, int64_t cols,
                                                          int gx) {
+    pdl_wait();  // inputs may be the previous kernel's output (PDL)
+    pdl_trigger();
     constexpr int VN = Vec32<T>::N;
     constexpr int U = 4;
     const int64_t chunk = blockIdx.x / gx;
@@ -149,7 +151,8 @@ template <class T> int diag_scale_impl(const lm_vec &dv, const lm_view &bv, int 
             const int64_t grid = gx * ceil_div(bv.cols, 4);
             if (grid <= 0x7fffffff) {
                 auto kern = side ? diag_scale_cols32<T, true> : diag_scale_cols32<T, false>;
-                kern<<<(unsigned)grid, 256, 0, s>>>(d, (const T *)bv.ptr, ldb, (T *)ov.ptr, ldo, bv.rows, bv.cols, gx);
+                LM_CUDA(launch_pdl(kern, dim3((unsigned)grid), dim3(256), 0, s, d, (const T *)bv.ptr, ldb, (T *)ov.ptr,
+                                   ldo, bv.rows, bv.cols, gx));
                 LM_LAUNCHED(1);
                 return 0;
             }
@@ -193,6 +196,8 @@ constexpr int kTr = 64;
 template <class T, bool CONTIG>
 __global__ void __launch_bounds__(kRedThreads, 2) trace_tiles(View<const T> A, View<const T> B, int64_t ntr,
                                                               int64_t ntiles, T *__restrict__ partials) {
+    pdl_wait();  // inputs may be the previous kernel's output (PDL)
+    pdl_trigger();
     __shared__ T sB[kTr][kTr + 1];
     __shared__ T red[kRedThreads / 32];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -319,6 +324,8 @@ __global__ void __launch_bounds__(kRedThreads, MINB) trace_quads(View<const T> A
 
 // Sum of `n` partials in index order, fixed tree; writes *out.
 template <class T> __global__ void __launch_bounds__(1024) sum_partials(const T *__restrict__ part, int64_t n, T *out) {
+    pdl_wait();  // inputs may be the previous kernel's output (PDL)
+    pdl_trigger();
     __shared__ T red[32];
     T acc = T(0);
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc = radd(acc, part[i]);
@@ -362,12 +369,12 @@ template <class T> int trace_impl(const lm_view &av, const lm_view &bv, void *d_
     Scratch part;
     if (int rc = part.alloc(sizeof(T) * blocks, s)) return rc;
     if (ntiles > 0) {
-        kern<<<(unsigned)blocks, kRedThreads, 0, s>>>(A, B, ntr, ntiles, part.as<T>());
+        LM_CUDA(launch_pdl(kern, dim3((unsigned)blocks), dim3(kRedThreads), 0, s, A, B, ntr, ntiles, part.as<T>()));
         LM_LAUNCHED(1);
     } else {
         LM_CUDA(cudaMemsetAsync(part.p, 0, sizeof(T), s));
     }
-    sum_partials<T><<<1, 1024, 0, s>>>(part.as<T>(), blocks, (T *)d_result);
+    LM_CUDA(launch_pdl(sum_partials<T>, dim3(1), dim3(1024), 0, s, (const T *)part.as<T>(), blocks, (T *)d_result));
     LM_LAUNCHED(1);
     return 0;
 }

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // runtime.cu -- library state: per-thread error text, launch counter,
 // device properties cache.
 #include <atomic>
@@ -35,6 +36,14 @@ void ensure_pool() {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     done[dev] = true;
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
 }
 
 int num_sms() {
