@@ -817,6 +817,220 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_f32(int64_t bat
     }
 }
 
+// n = 128 f32, "tc05": A.T @ B on the 5th-generation tensor cores --
+// tcgen05.mma kind::tf32 with the accumulator in TMEM, 3xTF32 (x = x_hi +
+// x_lo, a.b ~ a_hi b_lo + a_lo b_hi + a_hi b_hi; normwise ~1e-6, the north
+// star's f32 bar is 1e-5).  Warp-specialised, 2 CTAs per SM:
+//   warps 0-3 ("main"): stream 8-row chunks of A and B (and A's columns for
+//     the trace) through a 4-stage cp.async ring, split each chunk into TF32
+//     hi / lo operands in the UMMA canonical K-major layout (8 x 16 B core
+//     matrices, no swizzle), add the chunk's trace terms; thread 0 issues
+//     the three MMAs per chunk and commits them to mbarriers;
+//   warps 4-7 ("epilogue"): per instance, read the 128 x 128 accumulator
+//     from TMEM (tcgen05.ld, lane = row) and write E = round(P) + round(C*D)
+//     with coalesced column accesses -- overlapped with the next instance's
+//     main loop through two TMEM accumulators.
+// Descriptors and layouts checked by tools/tcgen05_tf32_probe.cu.
+constexpr int UKC = 8, UST = 4, UCB = 2;  // chunk rows, cp.async stages, split-operand buffers
+struct alignas(1024) SmemTc05 {
+    float conv[UCB][4][HN * UKC];   // [buf][a_hi, a_lo, b_hi, b_lo] core-matrix layout
+    float sa[UST][HN * UKC];        // A chunk: piece (m, kc) at 4 * (2m + kc)
+    float sb[UST][HN * UKC];        // B chunk: piece (n, kc)
+    float sac[UST][UKC * HN];       // A(i, k0 + k): [k][i]
+    float red[4];
+    float thalf[2];
+    uint32_t tmem_base;
+    unsigned long long mma_done[UCB], acc_full[2], acc_empty[2];
+};
+
+__device__ __forceinline__ uint64_t umma_desc(const void *p) {
+    // K-major, no swizzle: LBO = 128 B between the two 16-byte K pieces,
+    // SBO = 256 B between 8-row core-matrix groups; version 1 (Blackwell)
+    return (uint64_t)((sm_addr(p) >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+           (1ull << 46);
+}
+constexpr uint32_t kIdescTf32 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(HN >> 3) << 17) |
+                                ((uint32_t)(HN >> 4) << 24);
+__device__ __forceinline__ void umma_tf32(uint32_t tmem, uint64_t da, uint64_t db, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %3, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n}\n" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(acc), "r"(kIdescTf32));
+}
+__device__ __forceinline__ void umma_commit(unsigned long long *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sm_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+__device__ __forceinline__ int core_off(int r, int kc) { return (r >> 3) * 64 + kc * 32 + (r & 7) * 4; }  // floats
+
+__global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05(int64_t batch, const float *__restrict__ A,
+                                                               const float *__restrict__ B,
+                                                               const float *__restrict__ C,
+                                                               const float *__restrict__ D, float *__restrict__ E,
+                                                               float *__restrict__ S) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    SmemTc05 &sm = *reinterpret_cast<SmemTc05 *>(smraw);
+    constexpr int NCH = HN / UKC;  // 16 chunks per instance
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
+    const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_addr(&sm.tmem_base)),
+                     "r"(2 * HN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int q = 0; q < UCB; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.mma_done[q])));
+        for (int q = 0; q < 2; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.acc_full[q])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(sm_addr(&sm.acc_empty[q])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp < 4) {
+        // ---------------- main warps: stream, split, trace, MMA issue
+        const int t = tid;  // 0..127
+        auto stage = [&](int st, int64_t gch) {
+            const int64_t bi = blockIdx.x + (gch / NCH) * G;
+            const int k0 = (int)(gch % NCH) * UKC;
+            const float *pa = A + bi * nn, *pb = B + bi * nn;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int e = t + 128 * q, r = e >> 1, kc = e & 1;  // piece (row r, k piece kc)
+                cpa16(&sm.sa[st][4 * e], pa + (int64_t)r * HN + k0 + 4 * kc);
+                cpa16(&sm.sb[st][4 * e], pb + (int64_t)r * HN + k0 + 4 * kc);
+                const int kl = e >> 5, piece = e & 31;  // A's column k0 + kl, 16-byte piece
+                cpa16(&sm.sac[st][kl * HN + 4 * piece], pa + (int64_t)(k0 + kl) * HN + 4 * piece);
+            }
+        };
+        const int64_t total = J * NCH;
+#pragma unroll
+        for (int q = 0; q < UST - 1; ++q) {
+            if (q < total) stage(q, q);
+            cpa_commit();
+        }
+        float tr = 0.f;
+        for (int64_t g = 0; g < total; ++g) {
+            const int64_t j = g / NCH;
+            const int c = (int)(g % NCH);
+            const int st = (int)(g % UST), cb = (int)(g % UCB);
+            cpa_wait<UST - 2>();
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // chunk g visible; stage of g-1 free
+            if (g + UST - 1 < total) stage((int)((g + UST - 1) % UST), g + UST - 1);
+            cpa_commit();
+            // the MMAs that read conv[cb] (chunk g-UCB) must be done before it is rewritten
+            if (g >= UCB) mbar_wait(&sm.mma_done[cb], (unsigned)((g / UCB - 1) & 1));
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int e = t + 128 * q, r = e >> 1, kc = e & 1;
+                const float4 va = *reinterpret_cast<const float4 *>(&sm.sa[st][4 * e]);
+                const float4 vb = *reinterpret_cast<const float4 *>(&sm.sb[st][4 * e]);
+                float4 h, l;
+                h.x = tf32_rna(va.x); l.x = tf32_rna(va.x - h.x);
+                h.y = tf32_rna(va.y); l.y = tf32_rna(va.y - h.y);
+                h.z = tf32_rna(va.z); l.z = tf32_rna(va.z - h.z);
+                h.w = tf32_rna(va.w); l.w = tf32_rna(va.w - h.w);
+                *reinterpret_cast<float4 *>(&sm.conv[cb][0][core_off(r, kc)]) = h;
+                *reinterpret_cast<float4 *>(&sm.conv[cb][1][core_off(r, kc)]) = l;
+                h.x = tf32_rna(vb.x); l.x = tf32_rna(vb.x - h.x);
+                h.y = tf32_rna(vb.y); l.y = tf32_rna(vb.y - h.y);
+                h.z = tf32_rna(vb.z); l.z = tf32_rna(vb.z - h.z);
+                h.w = tf32_rna(vb.w); l.w = tf32_rna(vb.w - h.w);
+                *reinterpret_cast<float4 *>(&sm.conv[cb][2][core_off(r, kc)]) = h;
+                *reinterpret_cast<float4 *>(&sm.conv[cb][3][core_off(r, kc)]) = l;
+            }
+            {
+                // trace terms of the chunk: sum_k A(i, k) B(k, i), i = t; B(k0.., i) is piece (i, kc)
+                const float4 b0 = *reinterpret_cast<const float4 *>(&sm.sb[st][8 * t]);
+                const float4 b1 = *reinterpret_cast<const float4 *>(&sm.sb[st][8 * t + 4]);
+                const float *ac = sm.sac[st];
+                tr = fmaf(ac[0 * HN + t], b0.x, tr);
+                tr = fmaf(ac[1 * HN + t], b0.y, tr);
+                tr = fmaf(ac[2 * HN + t], b0.z, tr);
+                tr = fmaf(ac[3 * HN + t], b0.w, tr);
+                tr = fmaf(ac[4 * HN + t], b1.x, tr);
+                tr = fmaf(ac[5 * HN + t], b1.y, tr);
+                tr = fmaf(ac[6 * HN + t], b1.z, tr);
+                tr = fmaf(ac[7 * HN + t], b1.w, tr);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> MMA (async proxy)
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int ab = (int)(j & 1);
+            if (t == 0) {
+                if (c == 0 && j >= 2) mbar_wait(&sm.acc_empty[ab], (unsigned)(((j >> 1) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(ab * HN);
+                const uint64_t ah = umma_desc(sm.conv[cb][0]), al = umma_desc(sm.conv[cb][1]);
+                const uint64_t bh = umma_desc(sm.conv[cb][2]), bl = umma_desc(sm.conv[cb][3]);
+                umma_tf32(d, ah, bl, c > 0);
+                umma_tf32(d, al, bh, 1);
+                umma_tf32(d, ah, bh, 1);
+                umma_commit(&sm.mma_done[cb]);
+                if (c == NCH - 1) umma_commit(&sm.acc_full[ab]);
+            }
+            if (c == NCH - 1) {
+                // trace of instance j: fixed-order sum over the 128 main threads
+                tr = warp_sum(tr);
+                if (lane == 0) sm.red[warp] = tr;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (t == 0) S[blockIdx.x + j * G] = radd(radd(sm.red[0], sm.red[1]), radd(sm.red[2], sm.red[3]));
+                tr = 0.f;
+            }
+        }
+    } else {
+        // ---------------- epilogue warps: TMEM -> E = P + C % D
+        const int w4 = warp - 4, m = 32 * w4 + lane;
+        for (int64_t j = 0; j < J; ++j) {
+            const int ab = (int)(j & 1);
+            const int64_t b = blockIdx.x + j * G;
+            mbar_wait(&sm.acc_full[ab], (unsigned)((j >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float *pc = C + b * nn + m, *pd = D + b * nn + m;
+            float *pe = E + b * nn + m;
+            // 32 columns per step: 64 C / D loads in flight per thread (the
+            // epilogue is latency-bound with fewer), then the TMEM values
+#pragma unroll 1
+            for (int c0 = 0; c0 < HN; c0 += 32) {
+                float cv[32], dv[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    cv[q] = __ldcs(pc + (int64_t)(c0 + q) * HN);
+                    dv[q] = __ldcs(pd + (int64_t)(c0 + q) * HN);
+                }
+                uint32_t v[32];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                    : "r"(tmem + ((uint32_t)(32 * w4) << 16) + (uint32_t)(ab * HN + c0)));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    __stcs(pe + (int64_t)(c0 + q) * HN, radd(__uint_as_float(v[q]), rmul(cv[q], dv[q])));
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.acc_empty[ab])) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * HN));
+}
+
 }  // namespace
 
 // Generic fallback (any n): one CTA per instance, SIMT, 32 x 32 tiles.
@@ -878,6 +1092,21 @@ __global__ void __launch_bounds__(256) atb_schur_trace_generic(int64_t n, const 
         }
     tacc = block_sum<T, 256>(tacc, red);
     if (threadIdx.x == 0) S[b] = tacc;
+}
+
+int launch_tc05(int64_t batch, const float *a, const float *b, const float *c, const float *d, float *e, float *s,
+                cudaStream_t st) {
+    auto kern = atb_schur_trace_tc05;
+    const size_t smem = sizeof(SmemTc05) + 1024;  // + alignment slack
+    static int grid = 0;
+    if (!grid) {
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = resident_grid(kern, 256, smem);
+    }
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, 256, smem, st>>>(batch, a, b, c, d, e, s);
+    LM_LAUNCHED(1);
+    return 0;
 }
 
 int launch_stream_f32(int64_t batch, const float *a, const float *b, const float *c, const float *d, float *e,
@@ -987,6 +1216,8 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
             const char *v = getenv("LM_5A_TF32");  // 0: the FFMA kernel
             return !(v && v[0] == '0');
         }();
+        static const int tc05 = getenv("LM_5A_TC05") ? atoi(getenv("LM_5A_TC05")) : 1;
+        if (aligned && n == 128 && tf32x3 && tc05) return launch_tc05(batch, a, b, c, d, e, s, st);
         if (aligned && n == 128 && tf32x3) return launch_stream_f32(batch, a, b, c, d, e, s, st);
     }
     if (aligned && n == 128 && sizeof(T) == 8) return launch_half<T>(batch, a, b, c, d, e, s, st);
