@@ -72,16 +72,32 @@ __global__ void k(const float *A, const float *B, float *D, int passes) {
             const float4 va = *reinterpret_cast<const float4 *>(A + r * N + c * KC + kc * 4);
             const float4 vb = *reinterpret_cast<const float4 *>(B + r * N + c * KC + kc * 4);
             float4 h, l;
+            if (passes == 4) {  // hi = raw f32 (the MMA reads it as TF32), lo = x - truncated x
+                h = va;
+                l.x = va.x - __uint_as_float(__float_as_uint(va.x) & 0xffffe000u);
+                l.y = va.y - __uint_as_float(__float_as_uint(va.y) & 0xffffe000u);
+                l.z = va.z - __uint_as_float(__float_as_uint(va.z) & 0xffffe000u);
+                l.w = va.w - __uint_as_float(__float_as_uint(va.w) & 0xffffe000u);
+            } else {
             h.x = tf32r(va.x); l.x = tf32r(va.x - h.x);
             h.y = tf32r(va.y); l.y = tf32r(va.y - h.y);
             h.z = tf32r(va.z); l.z = tf32r(va.z - h.z);
             h.w = tf32r(va.w); l.w = tf32r(va.w - h.w);
+            }
             *reinterpret_cast<float4 *>(reinterpret_cast<char *>(ah) + core_off(r, kc)) = h;
             *reinterpret_cast<float4 *>(reinterpret_cast<char *>(al) + core_off(r, kc)) = l;
+            if (passes == 4) {
+                h = vb;
+                l.x = vb.x - __uint_as_float(__float_as_uint(vb.x) & 0xffffe000u);
+                l.y = vb.y - __uint_as_float(__float_as_uint(vb.y) & 0xffffe000u);
+                l.z = vb.z - __uint_as_float(__float_as_uint(vb.z) & 0xffffe000u);
+                l.w = vb.w - __uint_as_float(__float_as_uint(vb.w) & 0xffffe000u);
+            } else {
             h.x = tf32r(vb.x); l.x = tf32r(vb.x - h.x);
             h.y = tf32r(vb.y); l.y = tf32r(vb.y - h.y);
             h.z = tf32r(vb.z); l.z = tf32r(vb.z - h.z);
             h.w = tf32r(vb.w); l.w = tf32r(vb.w - h.w);
+            }
             *reinterpret_cast<float4 *>(reinterpret_cast<char *>(bh) + core_off(r, kc)) = h;
             *reinterpret_cast<float4 *>(reinterpret_cast<char *>(bl) + core_off(r, kc)) = l;
         }
@@ -91,7 +107,7 @@ __global__ void k(const float *A, const float *B, float *D, int passes) {
             asm volatile("tcgen05.fence::after_thread_sync;");
             const uint64_t dah = sdesc(ah, 128, 256), dal = sdesc(al, 128, 256);
             const uint64_t dbh = sdesc(bh, 128, 256), dbl = sdesc(bl, 128, 256);
-            if (passes == 3) {
+            if (passes >= 3) {
                 mma_tf32(tmem, dah, dbl, c > 0);
                 mma_tf32(tmem, dal, dbh, 1);
                 mma_tf32(tmem, dah, dbh, 1);
@@ -175,7 +191,7 @@ int main() {
     cudaMalloc(&dD, 4 * N * N);
     cudaMemcpy(dA, A.data(), 4 * N * N, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, B.data(), 4 * N * N, cudaMemcpyHostToDevice);
-    for (int passes : {1, 3}) {
+    for (int passes : {1, 3, 4}) {
         cudaMemset(dD, 0, 4 * N * N);
         k<<<1, 128>>>(dA, dB, dD, passes);
         cudaError_t e = cudaDeviceSynchronize();
