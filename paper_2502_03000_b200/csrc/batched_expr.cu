@@ -997,29 +997,27 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05(int64_t batch, co
             asm volatile("tcgen05.fence::after_thread_sync;");
             const float *pc = C + b * nn + m, *pd = D + b * nn + m;
             float *pe = E + b * nn + m;
-            // 32 columns per step: 64 C / D loads in flight per thread (the
-            // epilogue is latency-bound with fewer), then the TMEM values
+            // 16 columns per step (72 registers: two CTAs per SM; 32 columns per
+            // step needs 121 and leaves one)
 #pragma unroll 1
-            for (int c0 = 0; c0 < HN; c0 += 32) {
-                float cv[32], dv[32];
+            for (int c0 = 0; c0 < HN; c0 += 16) {
+                uint32_t v[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                    "[%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15])
+                    : "r"(tmem + ((uint32_t)(32 * w4) << 16) + (uint32_t)(ab * HN + c0)));
+                float cv[16], dv[16];
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
+                for (int q = 0; q < 16; ++q) {
                     cv[q] = __ldcs(pc + (int64_t)(c0 + q) * HN);
                     dv[q] = __ldcs(pd + (int64_t)(c0 + q) * HN);
                 }
-                uint32_t v[32];
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-                    "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-                      "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-                      "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-                      "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-                    : "r"(tmem + ((uint32_t)(32 * w4) << 16) + (uint32_t)(ab * HN + c0)));
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int q = 0; q < 32; ++q)
+                for (int q = 0; q < 16; ++q)
                     __stcs(pe + (int64_t)(c0 + q) * HN, radd(__uint_as_float(v[q]), rmul(cv[q], dv[q])));
             }
             asm volatile("tcgen05.fence::before_thread_sync;");
