@@ -18,6 +18,8 @@
 // and writes E; s is a fixed-order block reduction (deterministic).
 // Persistent CTAs loop over the instances of the class.
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <cstdlib>
 
@@ -612,6 +614,188 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream(int64_t batch, 
     }
 }
 
+// TMA variant of the stream kernel: each chunk arrives by two
+// cp.async.bulk.tensor.2d copies (A and B rows k0..k0+7 of the instance's 128
+// columns, box 8 x 128, dense 64-byte rows) and one 8 KB bulk copy (A's
+// columns), all issued by one thread and completed by transaction bytes;
+// the ring is 4 stages deep (3 chunks in flight) in the shared memory the
+// padded cp.async layout needed for 3.  tools/tma_stream_probe.cu streams
+// this access pattern at 6.5 TB/s.
+constexpr int TKC8 = 8, TST4 = 4;
+struct alignas(128) SmemStreamT {
+    double a[TST4][HN * TKC8];    // A(k, m): [m][k], dense
+    double b[TST4][HN * TKC8];    // B(k, n): [n][k]
+    double ac[TST4][TKC8 * HN];   // A(i, k): [k][i]
+    double p[HN * SLDP];          // previous instance's product: [n][m]
+    double red[16];
+    unsigned long long full[TST4], empty[TST4];
+};
+
+__global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t batch, const double *__restrict__ A,
+                                                                 const double *__restrict__ B,
+                                                                 const double *__restrict__ C,
+                                                                 const double *__restrict__ D, double *__restrict__ E,
+                                                                 double *__restrict__ S,
+                                                                     const __grid_constant__ CUtensorMap tmA,
+                                                                     const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SmemStreamT &sm = *reinterpret_cast<SmemStreamT *>(smraw);
+    constexpr int NCH = HN / TKC8;  // 16 chunks per instance
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
+    const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
+    // epilogue pair of this thread in chunk c: elements e, e+1 with e = 2*(c*512 + tid)
+    auto epi_off = [&](int c) -> int64_t {
+        const int e = 2 * (c * 512 + tid);
+        return (int64_t)e;  // column-major within the instance: n = e / 128, m = e % 128
+    };
+    auto p_off = [&](int c) -> int {
+        const int e = 2 * (c * 512 + tid), n = e >> 7, m = e & 127;
+        return n * SLDP + m;
+    };
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < TST4; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.full[q])), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.empty[q])), "r"(16));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // Ring without CTA-wide barriers: chunk g + TST4 - 1 is copied by warp
+    // g % 16 (a rotating producer) once every warp has released chunk g - 1
+    // (empty mbarrier); consumers wait only for their chunk's data (full
+    // mbarrier).  A barrier per chunk would line all warps up on the DMMA
+    // latency (tools/dmma_occ_probe.cu: a __syncthreads per 32 DMMAs per warp
+    // costs ~25% of the pipe).
+    const int64_t total = J * NCH;
+    // one thread per chunk issues two TMA tensor copies (A, B rows k0..k0+7 of
+    // the instance's 128 columns: box 8 x 128) and one 8 KB bulk copy (A's
+    // columns k0..k0+7); completion by transaction bytes on full[s]
+    auto produce = [&](int64_t gp) {
+        const int s = (int)(gp % TST4);
+        const int64_t u = gp / TST4;
+        if (u > 0) mbar_wait(&sm.empty[s], (unsigned)((u - 1) & 1));
+        const int64_t bi = blockIdx.x + (gp / NCH) * G;
+        const int k0 = (int)(gp % NCH) * TKC8;
+        const unsigned fb = sm_addr(&sm.full[s]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(3u * HN * TKC8 * 8u)
+                     : "memory");
+        const int c1 = (int)(bi * HN);
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                sm_addr(sm.a[s])),
+            "l"(&tmA), "r"(k0), "r"(c1), "r"(fb)
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                sm_addr(sm.b[s])),
+            "l"(&tmB), "r"(k0), "r"(c1), "r"(fb)
+            : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         sm_addr(sm.ac[s])),
+                     "l"(A + bi * nn + (int64_t)k0 * HN), "r"((unsigned)(HN * TKC8 * 8)), "r"(fb)
+                     : "memory");
+    };
+    // chunk g + TST4 - 1 is issued by lane 0 of warp g % 16 (rotating)
+    if (lane == 0 && warp < TST4 - 1 && warp < total) produce(warp);
+    int64_t gch = 0;  // global chunk counter (ring position)
+    int64_t b_cur = 0;
+    auto epi = [&](int c, double2 cv, double2 dv) {
+        const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[p_off(c)]);
+        double2 ev;
+        ev.x = radd(pv.x, rmul(cv.x, dv.x));
+        ev.y = radd(pv.y, rmul(cv.y, dv.y));
+        __stcs(reinterpret_cast<double2 *>(E + (b_cur - G) * nn + epi_off(c)), ev);
+    };
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t b = blockIdx.x + j * G;
+        b_cur = b;
+        const double *pa = A + b * nn, *pb = B + b * nn;
+        const bool prev = j > 0;
+        const int64_t bp = b - G;  // previous instance (valid when prev)
+        double acc[4][4][2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+        double tr = 0.0;
+        double2 cn_, dn_;  // C, D of the previous instance's pair for the next chunk
+        if (prev) {
+            cn_ = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(0)));
+            dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(0)));
+        }
+        for (int c = 0; c < NCH; ++c, ++gch) {
+            const int buf = (int)(gch % TST4);
+            if (lane == 0 && warp == (int)(gch % 16) && gch + TST4 - 1 < total) produce(gch + TST4 - 1);
+            __syncwarp();
+            double2 cv = cn_, dv = dn_;
+            if (prev && c + 1 < NCH) {
+                cn_ = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(c + 1)));
+                dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(c + 1)));
+            }
+            mbar_wait(&sm.full[buf], (unsigned)((gch / TST4) & 1));
+            const double *as = sm.a[buf];
+            const double *bs = sm.b[buf];
+#pragma unroll
+            for (int kk = 0; kk < TKC8; kk += 4) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * TKC8 + kk + fc];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + fr) * TKC8 + kk + fc];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) dmma884(acc[i][q], af[i], bf[q]);
+            }
+            {
+                // trace terms: sum_{k in chunk} sum_i A(i,k) B(k,i); 2 per thread
+                const double *ac = sm.ac[buf];
+                const int i = tid & 127, k2 = (tid >> 7) * 2;
+                tr = fma(ac[k2 * HN + i], bs[i * TKC8 + k2], tr);
+                tr = fma(ac[(k2 + 1) * HN + i], bs[i * TKC8 + k2 + 1], tr);
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.empty[buf])) : "memory");
+            if (prev) epi(c, cv, dv);
+        }
+        __syncthreads();  // every read of P (previous product) done
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) sm.p[(wn + q * 8 + 2 * fc + u) * SLDP + wm + i * 8 + fr] = acc[i][q][u];
+        // trace: fixed-order block sum
+        tr = warp_sum(tr);
+        if (lane == 0) sm.red[warp] = tr;
+        __syncthreads();
+        if (tid == 0) {
+            double t = sm.red[0];
+#pragma unroll
+            for (int q = 1; q < 16; ++q) t = radd(t, sm.red[q]);
+            S[b] = t;
+        }
+    }
+    if (J > 0) {
+        // drain: the last instance's epilogue
+        const int64_t bl = blockIdx.x + (J - 1) * G;
+#pragma unroll 4
+        for (int c = 0; c < NCH; ++c) {
+            const double2 cv = __ldcs(reinterpret_cast<const double2 *>(C + bl * nn + epi_off(c)));
+            const double2 dv = __ldcs(reinterpret_cast<const double2 *>(D + bl * nn + epi_off(c)));
+            const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[p_off(c)]);
+            double2 ev;
+            ev.x = radd(pv.x, rmul(cv.x, dv.x));
+            ev.y = radd(pv.y, rmul(cv.y, dv.y));
+            __stcs(reinterpret_cast<double2 *>(E + bl * nn + epi_off(c)), ev);
+        }
+    }
+}
+
 // n = 128 f32: the same streaming structure with A.T @ B on the TENSOR
 // cores in 3xTF32: every operand x is split into x_hi = tf32(x) and
 // x_lo = tf32(x - x_hi), and a.b is accumulated as a_hi b_lo + a_lo b_hi +
@@ -1122,6 +1306,49 @@ int launch_stream_f32(int64_t batch, const float *a, const float *b, const float
     return 0;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+        PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return f;
+    }();
+    return enc;
+}
+
+// batch x 128 x 128 column-major f64 instances as a 2D tensor: dim 0 = row
+// (contiguous), dim 1 = column over all instances; box 8 rows x 128 columns
+static bool rows_tensor_map(CUtensorMap *tm, const double *base, int64_t batch) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)HN, (cuuint64_t)(batch * HN)};
+    cuuint64_t strides[1] = {(cuuint64_t)HN * sizeof(double)};
+    cuuint32_t box[2] = {(cuuint32_t)TKC8, (cuuint32_t)HN};
+    cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int launch_stream_tma(int64_t batch, const double *a, const double *b, const double *c, const double *d, double *e,
+                      double *s, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    if (batch * HN > 0x7fffffff || !rows_tensor_map(&ta, a, batch) || !rows_tensor_map(&tb, b, batch)) return 1;
+    auto kern = atb_schur_trace_stream_tma;
+    const size_t smem = sizeof(SmemStreamT);
+    static int grid = 0;
+    if (!grid) {
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = resident_grid(kern, 512, smem);
+    }
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, 512, smem, st>>>(batch, a, b, c, d, e, s, ta, tb);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
 int launch_stream(int64_t batch, const double *a, const double *b, const double *c, const double *d, double *e,
                   double *s, cudaStream_t st) {
     auto kern = atb_schur_trace_stream;
@@ -1208,6 +1435,11 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
         return !(v && v[0] == '0');
     }();
     if constexpr (sizeof(T) == 8) {
+        static const int tma = getenv("LM_5A_TMA") ? atoi(getenv("LM_5A_TMA")) : 1;
+        if (aligned && n == 128 && stream128 && tma) {
+            const int rc = launch_stream_tma(batch, a, b, c, d, e, s, st);
+            if (rc <= 0) return rc;  // 1: no tensor-map encoder -> the cp.async ring
+        }
         if (aligned && n == 128 && stream128) return launch_stream(batch, a, b, c, d, e, s, st);
     } else {
         static const bool tf32x3 = [] {
