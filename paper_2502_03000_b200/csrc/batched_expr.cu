@@ -1213,6 +1213,190 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05(int64_t batch, co
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * HN));
 }
 
+// tcgen05 f32 kernel fed by TMA: every chunk arrives as four
+// cp.async.bulk.tensor.2d copies (A and B, k pieces 0 / 1: box 4 floats x 128
+// rows -- each lands as one 2 KB plane of 16-byte rows, so the chunk is
+// already in the UMMA K-major core-matrix layout: SBO = 128 B, LBO = 2 KB)
+// plus one 4 KB bulk copy of A's columns, issued by one thread.  The raw f32
+// chunk is the TF32 hi operand (the MMA reads the top 19 bits; measured
+// 1.5e-6 normwise with lo = x - trunc_tf32(x)), so the main warps only form
+// the lo operands, the trace terms and the MMA issue.  Six stages, four chunks
+// in flight, a stage is refilled once the MMAs of the chunk two back finished.
+constexpr int VKC = 8, VST = 6, VAHEAD = 4;
+struct alignas(1024) SmemTc05T {
+    float sa[VST][HN * VKC];   // A chunk (= a_hi): [kc][m][4]
+    float sb[VST][HN * VKC];   // B chunk (= b_hi)
+    float lo[2][2][HN * VKC];  // [buf][a_lo, b_lo], same layout
+    float sac[VST][VKC * HN];  // A(i, k0 + k): [k][i]
+    float red[4];
+    uint32_t tmem_base;
+    unsigned long long full[VST], mma_done[VST], acc_full[2], acc_empty[2];
+};
+
+__device__ __forceinline__ uint64_t umma_desc_planes(const void *p) {
+    // K-major, no swizzle: 8-row core-matrix groups 128 B apart (SBO), the two
+    // 16-byte K pieces in 2 KB planes (LBO); version 1
+    return (uint64_t)((sm_addr(p) >> 4) & 0x3FFF) | ((uint64_t)(2048 >> 4) << 16) | ((uint64_t)(128 >> 4) << 32) |
+           (1ull << 46);
+}
+
+__global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05t(int64_t batch, const float *__restrict__ A,
+                                                                const float *__restrict__ C,
+                                                                const float *__restrict__ D, float *__restrict__ E,
+                                                                float *__restrict__ S,
+                                                                const __grid_constant__ CUtensorMap tmA,
+                                                                const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    SmemTc05T &sm = *reinterpret_cast<SmemTc05T *>(smraw + ((1024 - (sm_addr(smraw) & 1023)) & 1023));
+    constexpr int NCH = HN / VKC;  // 16 chunks per instance
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
+    const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_addr(&sm.tmem_base)),
+                     "r"(2 * HN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int q = 0; q < VST; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.full[q])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.mma_done[q])));
+        }
+        for (int q = 0; q < 2; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.acc_full[q])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(sm_addr(&sm.acc_empty[q])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp < 4) {
+        const int t = tid;
+        const int64_t total = J * NCH;
+        auto produce = [&](int64_t gp) {
+            const int st = (int)(gp % VST);
+            const int64_t bi = blockIdx.x + (gp / NCH) * G;
+            const int k0 = (int)(gp % NCH) * VKC, m0 = (int)(bi * HN);
+            const unsigned fb = sm_addr(&sm.full[st]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(3u * HN * VKC * 4u)
+                         : "memory");
+#pragma unroll
+            for (int kc = 0; kc < 2; ++kc) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];" ::"r"(sm_addr(&sm.sa[st][kc * HN * 4])),
+                    "l"(&tmA), "r"(k0 + 4 * kc), "r"(m0), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];" ::"r"(sm_addr(&sm.sb[st][kc * HN * 4])),
+                    "l"(&tmB), "r"(k0 + 4 * kc), "r"(m0), "r"(fb)
+                    : "memory");
+            }
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             sm_addr(sm.sac[st])),
+                         "l"(A + bi * nn + (int64_t)k0 * HN), "r"((unsigned)(HN * VKC * 4)), "r"(fb)
+                         : "memory");
+        };
+        if (t == 0)
+            for (int64_t q = 0; q < VAHEAD && q < total; ++q) produce(q);
+        float tr = 0.f;
+        for (int64_t g = 0; g < total; ++g) {
+            const int64_t j = g / NCH;
+            const int c = (int)(g % NCH);
+            const int st = (int)(g % VST), lb = (int)(g & 1);
+            mbar_wait(&sm.full[st], (unsigned)((g / VST) & 1));
+            // chunk g-2's MMAs read lo[lb] and the stage chunk g+VAHEAD refills
+            if (g >= 2) mbar_wait(&sm.mma_done[(g - 2) % VST], (unsigned)(((g - 2) / VST) & 1));
+            if (t == 0 && g + VAHEAD < total) produce(g + VAHEAD);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int o = 4 * (t + 128 * q);  // piece (m = t, kc = q): plane q, row t
+                const float4 va = *reinterpret_cast<const float4 *>(&sm.sa[st][o]);
+                const float4 vb = *reinterpret_cast<const float4 *>(&sm.sb[st][o]);
+                float4 la, lv;
+                la.x = va.x - __uint_as_float(__float_as_uint(va.x) & 0xffffe000u);
+                la.y = va.y - __uint_as_float(__float_as_uint(va.y) & 0xffffe000u);
+                la.z = va.z - __uint_as_float(__float_as_uint(va.z) & 0xffffe000u);
+                la.w = va.w - __uint_as_float(__float_as_uint(va.w) & 0xffffe000u);
+                lv.x = vb.x - __uint_as_float(__float_as_uint(vb.x) & 0xffffe000u);
+                lv.y = vb.y - __uint_as_float(__float_as_uint(vb.y) & 0xffffe000u);
+                lv.z = vb.z - __uint_as_float(__float_as_uint(vb.z) & 0xffffe000u);
+                lv.w = vb.w - __uint_as_float(__float_as_uint(vb.w) & 0xffffe000u);
+                *reinterpret_cast<float4 *>(&sm.lo[lb][0][o]) = la;
+                *reinterpret_cast<float4 *>(&sm.lo[lb][1][o]) = lv;
+                // trace terms: B(k0 + 4q + x, i = t) * A(i, k0 + 4q + x)
+                const float *ac = &sm.sac[st][(4 * q) * HN + t];
+                tr = fmaf(ac[0], vb.x, tr);
+                tr = fmaf(ac[HN], vb.y, tr);
+                tr = fmaf(ac[2 * HN], vb.z, tr);
+                tr = fmaf(ac[3 * HN], vb.w, tr);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int ab = (int)(j & 1);
+            if (t == 0) {
+                if (c == 0 && j >= 2) mbar_wait(&sm.acc_empty[ab], (unsigned)(((j >> 1) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(ab * HN);
+                const uint64_t ah = umma_desc_planes(sm.sa[st]), al = umma_desc_planes(sm.lo[lb][0]);
+                const uint64_t bh = umma_desc_planes(sm.sb[st]), bl = umma_desc_planes(sm.lo[lb][1]);
+                umma_tf32(d, ah, bl, c > 0);
+                umma_tf32(d, al, bh, 1);
+                umma_tf32(d, ah, bh, 1);
+                umma_commit(&sm.mma_done[st]);
+                if (c == NCH - 1) umma_commit(&sm.acc_full[ab]);
+            }
+            if (c == NCH - 1) {
+                tr = warp_sum(tr);
+                if (lane == 0) sm.red[warp] = tr;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (t == 0) S[blockIdx.x + j * G] = radd(radd(sm.red[0], sm.red[1]), radd(sm.red[2], sm.red[3]));
+                tr = 0.f;
+            }
+        }
+    } else {
+        const int w4 = warp - 4, m = 32 * w4 + lane;
+        for (int64_t j = 0; j < J; ++j) {
+            const int ab = (int)(j & 1);
+            const int64_t b = blockIdx.x + j * G;
+            mbar_wait(&sm.acc_full[ab], (unsigned)((j >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const float *pc = C + b * nn + m, *pd = D + b * nn + m;
+            float *pe = E + b * nn + m;
+#pragma unroll 1
+            for (int c0 = 0; c0 < HN; c0 += 16) {
+                uint32_t v[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                    "[%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15])
+                    : "r"(tmem + ((uint32_t)(32 * w4) << 16) + (uint32_t)(ab * HN + c0)));
+                float cv[16], dv[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    cv[q] = __ldcs(pc + (int64_t)(c0 + q) * HN);
+                    dv[q] = __ldcs(pd + (int64_t)(c0 + q) * HN);
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    __stcs(pe + (int64_t)(c0 + q) * HN, radd(__uint_as_float(v[q]), rmul(cv[q], dv[q])));
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.acc_empty[ab])) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * HN));
+}
+
 }  // namespace
 
 // Generic fallback (any n): one CTA per instance, SIMT, 32 x 32 tiles.
@@ -1349,6 +1533,39 @@ int launch_stream_tma(int64_t batch, const double *a, const double *b, const dou
     return 0;
 }
 
+// batch x 128 x 128 column-major f32 instances as a 2D tensor: dim 0 = row k
+// (contiguous, 128), dim 1 = column over all instances; box 4 rows x 128
+// columns (one 16-byte K piece of every column)
+static bool planes_tensor_map(CUtensorMap *tm, const float *base, int64_t batch) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)HN, (cuuint64_t)(batch * HN)};
+    cuuint64_t strides[1] = {(cuuint64_t)HN * sizeof(float)};
+    cuuint32_t box[2] = {4, (cuuint32_t)HN};
+    cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int launch_tc05t(int64_t batch, const float *a, const float *b, const float *c, const float *d, float *e, float *s,
+                 cudaStream_t st) {
+    CUtensorMap ta, tb;
+    if (batch * HN > 0x7fffffff || !planes_tensor_map(&ta, a, batch) || !planes_tensor_map(&tb, b, batch)) return 1;
+    auto kern = atb_schur_trace_tc05t;
+    const size_t smem = sizeof(SmemTc05T) + 1024;
+    static int grid = 0;
+    if (!grid) {
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        grid = resident_grid(kern, 256, smem);
+    }
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, 256, smem, st>>>(batch, a, c, d, e, s, ta, tb);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
+
 int launch_stream(int64_t batch, const double *a, const double *b, const double *c, const double *d, double *e,
                   double *s, cudaStream_t st) {
     auto kern = atb_schur_trace_stream;
@@ -1446,7 +1663,11 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
             const char *v = getenv("LM_5A_TF32");  // 0: the FFMA kernel
             return !(v && v[0] == '0');
         }();
-        static const int tc05 = getenv("LM_5A_TC05") ? atoi(getenv("LM_5A_TC05")) : 1;
+        static const int tc05 = getenv("LM_5A_TC05") ? atoi(getenv("LM_5A_TC05")) : 2;  // 2: TMA-fed, 1: cp.async-fed
+        if (aligned && n == 128 && tf32x3 && tc05 >= 2) {
+            const int rc = launch_tc05t(batch, a, b, c, d, e, s, st);
+            if (rc <= 0) return rc;
+        }
         if (aligned && n == 128 && tf32x3 && tc05) return launch_tc05(batch, a, b, c, d, e, s, st);
         if (aligned && n == 128 && tf32x3) return launch_stream_f32(batch, a, b, c, d, e, s, st);
     }
