@@ -1467,7 +1467,8 @@ int launch_tc05(int64_t batch, const float *a, const float *b, const float *c, c
     static int grid = 0;
     if (!grid) {
         LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = resident_grid(kern, 256, smem);
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        grid = 2 * num_sms();  // two CTAs per SM fit; the occupancy API answers 1 (see launch_tc05t)
     }
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 256, smem, st>>>(batch, a, b, c, d, e, s);
@@ -1557,7 +1558,13 @@ int launch_tc05t(int64_t batch, const float *a, const float *b, const float *c, 
     static int grid = 0;
     if (!grid) {
         LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = resident_grid(kern, 256, smem);
+        // the whole unified L1/shared array as shared memory: without it the
+        // carveout chosen for one CTA leaves the SM at one CTA (ncu: grid 148)
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        // two CTAs per SM fit (ncu: shared-memory limit 2, registers 3) but the
+        // occupancy API answers 1 for this kernel; LM_TC05_CTAS overrides
+        static const int per = getenv("LM_TC05_CTAS") ? atoi(getenv("LM_TC05_CTAS")) : 2;
+        grid = per * num_sms();
     }
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 256, smem, st>>>(batch, a, c, d, e, s, ta, tb);
