@@ -1,0 +1,58 @@
+"""The n = 128 batched-expression kernels have A/B baselines behind
+environment switches (read once per process): TMA-fed vs cp.async-fed rings,
+tcgen05 vs legacy mma.sync TF32, the streaming vs the two-CTA cluster f64
+kernel.  Each variant runs in a subprocess on the same seeded batch and must
+agree with the oracle-checked default within the north-star tolerance."""
+import json
+import os
+import pathlib
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = pathlib.Path(__file__).resolve().parents[1]
+SCRIPT = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2502_03000_b200.batch import atb_schur_trace, stack_fortran
+dt = torch.float64 if sys.argv[2] == "f64" else torch.float32
+rng = np.random.default_rng(11)
+bt, n = 400, 128
+ops = [rng.uniform(-1, 1, (bt, n, n)) for _ in range(4)]
+E, s = atb_schur_trace(*(stack_fortran(o, dtype=dt) for o in ops))
+idx = [0, 1, 147, 148, 296, 299, 399]
+print(json.dumps({"E": E[idx].double().cpu().numpy().ravel()[::97].tolist(), "s": s[idx].double().cpu().tolist()}))
+"""
+
+
+def run(env_extra, dtype):
+    env = dict(os.environ)
+    env.update(env_extra)
+    out = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), dtype], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def close(a, b, tol):
+    import numpy as np
+    a, b = np.asarray(a), np.asarray(b)
+    return np.max(np.abs(a - b)) <= tol * max(np.max(np.abs(b)), 1e-30)
+
+
+@pytest.mark.parametrize("variant", [{"LM_5A_TMA": "0"}, {"LM_5A_STREAM": "0"}])
+def test_f64_variants_agree(variant):
+    ref = run({}, "f64")
+    got = run(variant, "f64")
+    assert close(got["E"], ref["E"], 1e-12) and close(got["s"], ref["s"], 1e-12)
+
+
+@pytest.mark.parametrize("variant", [{"LM_5A_TC05": "1"}, {"LM_5A_TC05": "0"}, {"LM_5A_TF32": "0"}])
+def test_f32_variants_agree(variant):
+    ref = run({}, "f32")
+    got = run(variant, "f32")
+    assert close(got["E"], ref["E"], 1e-5) and close(got["s"], ref["s"], 1e-5)
