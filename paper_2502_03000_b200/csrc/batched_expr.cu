@@ -1397,6 +1397,174 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05t(int64_t batch, c
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * HN));
 }
 
+__global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05p(int64_t batch, const float *__restrict__ A,
+                                                                const float *__restrict__ C,
+                                                                const float *__restrict__ D, float *__restrict__ E,
+                                                                float *__restrict__ S,
+                                                                const __grid_constant__ CUtensorMap tmA,
+                                                                const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    SmemTc05T &sm = *reinterpret_cast<SmemTc05T *>(smraw + ((1024 - (sm_addr(smraw) & 1023)) & 1023));
+    // n = 64: instances 2p and 2p+1 side by side -- the MMA computes
+    // [A_2p | A_2p+1].T @ [B_2p | B_2p+1] (128 x 128, K = 64) and only the two
+    // diagonal 64 x 64 blocks are kept (the tensor cores have the slack)
+    constexpr int PN = 64, NCH = PN / VKC;  // 8 chunks per pair
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nn = (int64_t)PN * PN, G = gridDim.x, npairs = (batch + 1) / 2;
+    const int64_t J = npairs > (int64_t)blockIdx.x ? (npairs - blockIdx.x + G - 1) / G : 0;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_addr(&sm.tmem_base)),
+                     "r"(2 * HN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        for (int q = 0; q < VST; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.full[q])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.mma_done[q])));
+        }
+        for (int q = 0; q < 2; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_addr(&sm.acc_full[q])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(sm_addr(&sm.acc_empty[q])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = sm.tmem_base;
+
+    if (warp < 4) {
+        const int t = tid;
+        const int64_t total = J * NCH;
+        auto produce = [&](int64_t gp) {
+            const int st = (int)(gp % VST);
+            const int64_t pi = blockIdx.x + (gp / NCH) * G;
+            const int k0 = (int)(gp % NCH) * VKC, m0 = (int)(pi * 2 * PN);
+            const bool two = 2 * pi + 1 < batch;
+            const unsigned fb = sm_addr(&sm.full[st]);
+            // A and B planes: always 2 x 2 x 2 KB (TMA zero-fills a missing second
+            // instance); A's columns: 2 KB per instance present
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                         "r"(2u * HN * VKC * 4u + (two ? 2u : 1u) * PN * VKC * 4u)
+                         : "memory");
+#pragma unroll
+            for (int kc = 0; kc < 2; ++kc) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];" ::"r"(sm_addr(&sm.sa[st][kc * HN * 4])),
+                    "l"(&tmA), "r"(k0 + 4 * kc), "r"(m0), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                    "[%4];" ::"r"(sm_addr(&sm.sb[st][kc * HN * 4])),
+                    "l"(&tmB), "r"(k0 + 4 * kc), "r"(m0), "r"(fb)
+                    : "memory");
+            }
+            for (int q = 0; q < (two ? 2 : 1); ++q)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 sm_addr(&sm.sac[st][q * PN * VKC])),
+                             "l"(A + (2 * pi + q) * nn + (int64_t)k0 * PN), "r"((unsigned)(PN * VKC * 4)), "r"(fb)
+                             : "memory");
+        };
+        if (t == 0)
+            for (int64_t q = 0; q < VAHEAD && q < total; ++q) produce(q);
+        float tr = 0.f;
+        for (int64_t g = 0; g < total; ++g) {
+            const int64_t j = g / NCH;
+            const int c = (int)(g % NCH);
+            const int st = (int)(g % VST), lb = (int)(g & 1);
+            mbar_wait(&sm.full[st], (unsigned)((g / VST) & 1));
+            // chunk g-2's MMAs read lo[lb] and the stage chunk g+VAHEAD refills
+            if (g >= 2) mbar_wait(&sm.mma_done[(g - 2) % VST], (unsigned)(((g - 2) / VST) & 1));
+            if (t == 0 && g + VAHEAD < total) produce(g + VAHEAD);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int o = 4 * (t + 128 * q);  // piece (m = t, kc = q): plane q, row t
+                const float4 va = *reinterpret_cast<const float4 *>(&sm.sa[st][o]);
+                const float4 vb = *reinterpret_cast<const float4 *>(&sm.sb[st][o]);
+                float4 la, lv;
+                la.x = va.x - __uint_as_float(__float_as_uint(va.x) & 0xffffe000u);
+                la.y = va.y - __uint_as_float(__float_as_uint(va.y) & 0xffffe000u);
+                la.z = va.z - __uint_as_float(__float_as_uint(va.z) & 0xffffe000u);
+                la.w = va.w - __uint_as_float(__float_as_uint(va.w) & 0xffffe000u);
+                lv.x = vb.x - __uint_as_float(__float_as_uint(vb.x) & 0xffffe000u);
+                lv.y = vb.y - __uint_as_float(__float_as_uint(vb.y) & 0xffffe000u);
+                lv.z = vb.z - __uint_as_float(__float_as_uint(vb.z) & 0xffffe000u);
+                lv.w = vb.w - __uint_as_float(__float_as_uint(vb.w) & 0xffffe000u);
+                *reinterpret_cast<float4 *>(&sm.lo[lb][0][o]) = la;
+                *reinterpret_cast<float4 *>(&sm.lo[lb][1][o]) = lv;
+                // trace terms of instance 2p + (t >> 6), i = t & 63: B(k, i) * A(i, k)
+                const float *ac = &sm.sac[st][(t >> 6) * PN * VKC + (4 * q) * PN + (t & 63)];
+                tr = fmaf(ac[0], vb.x, tr);
+                tr = fmaf(ac[PN], vb.y, tr);
+                tr = fmaf(ac[2 * PN], vb.z, tr);
+                tr = fmaf(ac[3 * PN], vb.w, tr);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int ab = (int)(j & 1);
+            if (t == 0) {
+                if (c == 0 && j >= 2) mbar_wait(&sm.acc_empty[ab], (unsigned)(((j >> 1) - 1) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t d = tmem + (uint32_t)(ab * HN);
+                const uint64_t ah = umma_desc_planes(sm.sa[st]), al = umma_desc_planes(sm.lo[lb][0]);
+                const uint64_t bh = umma_desc_planes(sm.sb[st]), bl = umma_desc_planes(sm.lo[lb][1]);
+                umma_tf32(d, ah, bl, c > 0);
+                umma_tf32(d, al, bh, 1);
+                umma_tf32(d, ah, bh, 1);
+                umma_commit(&sm.mma_done[st]);
+                if (c == NCH - 1) umma_commit(&sm.acc_full[ab]);
+            }
+            if (c == NCH - 1) {
+                tr = warp_sum(tr);
+                if (lane == 0) sm.red[warp] = tr;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const int64_t pj = blockIdx.x + j * G;
+                if (t == 0) S[2 * pj] = radd(sm.red[0], sm.red[1]);
+                if (t == 64 && 2 * pj + 1 < batch) S[2 * pj + 1] = radd(sm.red[2], sm.red[3]);
+                tr = 0.f;
+            }
+        }
+    } else {
+        const int w4 = warp - 4, half = w4 >> 1, m = 32 * (w4 & 1) + lane;  // TMEM lane 32*w4 + lane
+        for (int64_t j = 0; j < J; ++j) {
+            const int ab = (int)(j & 1);
+            const int64_t b = 2 * (blockIdx.x + j * G) + half;  // this warp's instance of the pair
+            mbar_wait(&sm.acc_full[ab], (unsigned)((j >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const bool live = b < batch;
+            const float *pc = C + b * nn + m, *pd = D + b * nn + m;
+            float *pe = E + b * nn + m;
+#pragma unroll 1
+            for (int c0 = 0; c0 < (live ? PN : 0); c0 += 16) {
+                uint32_t v[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                    "[%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                      "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                      "=r"(v[15])
+                    : "r"(tmem + ((uint32_t)(32 * w4) << 16) + (uint32_t)(ab * HN + half * PN + c0)));
+                float cv[16], dv[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    cv[q] = __ldcs(pc + (int64_t)(c0 + q) * PN);
+                    dv[q] = __ldcs(pd + (int64_t)(c0 + q) * PN);
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    __stcs(pe + (int64_t)(c0 + q) * PN, radd(__uint_as_float(v[q]), rmul(cv[q], dv[q])));
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.acc_empty[ab])) : "memory");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * HN));
+}
+
 }  // namespace
 
 // Generic fallback (any n): one CTA per instance, SIMT, 32 x 32 tiles.
@@ -1549,6 +1717,40 @@ static bool planes_tensor_map(CUtensorMap *tm, const float *base, int64_t batch)
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// n = 64 pairs: 2D view with 64-row columns; box 4 rows x 128 columns = one
+// 16-byte K piece of both instances of a pair
+static bool pair_planes_tensor_map(CUtensorMap *tm, const float *base, int64_t batch) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {64, (cuuint64_t)(batch * 64)};
+    cuuint64_t strides[1] = {64 * sizeof(float)};
+    cuuint32_t box[2] = {4, 128};
+    cuuint32_t es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int launch_tc05p(int64_t batch, const float *a, const float *b, const float *c, const float *d, float *e, float *s,
+                 cudaStream_t st) {
+    CUtensorMap ta, tb;
+    if (batch * 64 > 0x7fffffff || !pair_planes_tensor_map(&ta, a, batch) || !pair_planes_tensor_map(&tb, b, batch))
+        return 1;
+    auto kern = atb_schur_trace_tc05p;
+    const size_t smem = sizeof(SmemTc05T) + 1024;
+    static int grid = 0;
+    if (!grid) {
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        grid = 2 * num_sms();  // as launch_tc05t
+    }
+    const int64_t np = (batch + 1) / 2;
+    const int64_t g = np < grid ? np : grid;
+    kern<<<(unsigned)g, 256, smem, st>>>(batch, a, c, d, e, s, ta, tb);
+    LM_LAUNCHED(1);
+    return 0;
+}
+
 int launch_tc05t(int64_t batch, const float *a, const float *b, const float *c, const float *d, float *e, float *s,
                  cudaStream_t st) {
     CUtensorMap ta, tb;
@@ -1651,6 +1853,13 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
                       cudaStream_t st) {
     const bool aligned = ((uintptr_t)a | (uintptr_t)b) % 16 == 0;
     if (aligned && n == 32) return launch_tc<T, 32>(batch, a, b, c, d, e, s, st);
+    if constexpr (sizeof(T) == 4) {
+        static const int p64 = getenv("LM_5A_TC05P") ? atoi(getenv("LM_5A_TC05P")) : 1;
+        if (aligned && n == 64 && p64) {
+            const int rc = launch_tc05p(batch, a, b, c, d, e, s, st);
+            if (rc <= 0) return rc;
+        }
+    }
     if (aligned && n == 64) return launch_tc<T, 64>(batch, a, b, c, d, e, s, st);
     // n = 128: the two-CTA split wins for f64 (17.6 vs 19.7 ms on config 5a's
     // 87k instances); FP32 keeps the one-CTA kernel (10.0 vs 11.7 ms)

@@ -130,7 +130,7 @@ def test_atb_schur_trace_many_instances_per_cta(n, dtype):
     finished during instance j+1's main loop) and its drain are exercised;
     sampled instances against the oracle."""
     rng = np.random.default_rng(7 * n)
-    bt = 700
+    bt = 701  # odd: the paired n = 64 kernel's last pair has one instance
     ops = [rng.uniform(-1, 1, (bt, n, n)) for _ in range(4)]
     if dtype == torch.float32:
         ops = [o.astype(np.float32).astype(np.float64) for o in ops]
@@ -138,7 +138,7 @@ def test_atb_schur_trace_many_instances_per_cta(n, dtype):
     E, s = E.cpu().numpy(), s.cpu().numpy()
     pops, pargs, *_ = parse_program("x0 x1 x2 * +")
     tol = 1e-12 if dtype == torch.float64 else 1e-5
-    for i in sorted({0, 1, 147, 148, 149, 295, 296, 297, 443, 444, 591, 592, 699, int(rng.integers(0, bt))}):
+    for i in sorted({0, 1, 147, 148, 149, 295, 296, 297, 443, 444, 591, 592, 699, 700, int(rng.integers(0, bt))}):
         A, B, C, D = (np.asfortranarray(o[i]) for o in ops)
         g = np.zeros((n, n), order="F")
         O.gemm(A.T, B, g)
