@@ -639,11 +639,15 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
                                                                      const __grid_constant__ CUtensorMap tmA,
                                                                      const __grid_constant__ CUtensorMap tmB) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    SmemStreamT &sm = *reinterpret_cast<SmemStreamT *>(smraw);
+    // 512-byte aligned base: the TMA 64-byte swizzle repeats every 512 B
+    SmemStreamT &sm = *reinterpret_cast<SmemStreamT *>(smraw + ((512 - (sm_addr(smraw) & 511)) & 511));
     constexpr int NCH = HN / TKC8;  // 16 chunks per instance
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
     const int fr = lane >> 2, fc = lane & 3;
+    // TMA SWIZZLE_64B: 16-byte chunk c of row m lands at chunk c ^ ((m >> 1) & 3);
+    // rows wm + 8i + fr share (m >> 1) & 3 = (fr >> 1) & 3
+    const int sw0 = (((fc >> 1) ^ ((fr >> 1) & 3)) << 1) + (fc & 1), sw4 = sw0 ^ 4;
     const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
     const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
     // epilogue pair of this thread in chunk c: elements e, e+1 with e = 2*(c*512 + tid)
@@ -742,10 +746,11 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
 #pragma unroll
             for (int kk = 0; kk < TKC8; kk += 4) {
                 double af[4], bf[4];
+                const int o = kk ? sw4 : sw0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * TKC8 + kk + fc];
+                for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * TKC8 + o];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + fr) * TKC8 + kk + fc];
+                for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + fr) * TKC8 + o];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -755,8 +760,9 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
                 // trace terms: sum_{k in chunk} sum_i A(i,k) B(k,i); 2 per thread
                 const double *ac = sm.ac[buf];
                 const int i = tid & 127, k2 = (tid >> 7) * 2;
-                tr = fma(ac[k2 * HN + i], bs[i * TKC8 + k2], tr);
-                tr = fma(ac[(k2 + 1) * HN + i], bs[i * TKC8 + k2 + 1], tr);
+                const int bo = i * TKC8 + (((k2 >> 1) ^ ((i >> 1) & 3)) << 1);  // k2 even
+                tr = fma(ac[k2 * HN + i], bs[bo], tr);
+                tr = fma(ac[(k2 + 1) * HN + i], bs[bo + 1], tr);
             }
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.empty[buf])) : "memory");
@@ -1681,7 +1687,7 @@ static bool rows_tensor_map(CUtensorMap *tm, const double *base, int64_t batch) 
     cuuint32_t box[2] = {(cuuint32_t)TKC8, (cuuint32_t)HN};
     cuuint32_t es[2] = {1, 1};
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1690,7 +1696,7 @@ int launch_stream_tma(int64_t batch, const double *a, const double *b, const dou
     CUtensorMap ta, tb;
     if (batch * HN > 0x7fffffff || !rows_tensor_map(&ta, a, batch) || !rows_tensor_map(&tb, b, batch)) return 1;
     auto kern = atb_schur_trace_stream_tma;
-    const size_t smem = sizeof(SmemStreamT);
+    const size_t smem = sizeof(SmemStreamT) + 512;  // + alignment slack
     static int grid = 0;
     if (!grid) {
         LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
