@@ -1403,6 +1403,7 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05t(int64_t batch, c
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * HN));
 }
 
+template <int PN>
 __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05p(int64_t batch, const float *__restrict__ A,
                                                                 const float *__restrict__ C,
                                                                 const float *__restrict__ D, float *__restrict__ E,
@@ -1411,12 +1412,12 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05p(int64_t batch, c
                                                                 const __grid_constant__ CUtensorMap tmB) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     SmemTc05T &sm = *reinterpret_cast<SmemTc05T *>(smraw + ((1024 - (sm_addr(smraw) & 1023)) & 1023));
-    // n = 64: instances 2p and 2p+1 side by side -- the MMA computes
-    // [A_2p | A_2p+1].T @ [B_2p | B_2p+1] (128 x 128, K = 64) and only the two
-    // diagonal 64 x 64 blocks are kept (the tensor cores have the slack)
-    constexpr int PN = 64, NCH = PN / VKC;  // 8 chunks per pair
+    // n = PN (64 or 32): NPER = 128 / PN instances side by side -- the MMA
+    // computes [A_0 | A_1 ..].T @ [B_0 | B_1 ..] (128 x 128, K = PN) and only
+    // the diagonal PN x PN blocks are kept (the tensor cores have the slack)
+    constexpr int NPER = HN / PN, NCH = PN / VKC, WPI = PN / 32;  // warps per instance (trace, epilogue)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t nn = (int64_t)PN * PN, G = gridDim.x, npairs = (batch + 1) / 2;
+    const int64_t nn = (int64_t)PN * PN, G = gridDim.x, npairs = (batch + NPER - 1) / NPER;
     const int64_t J = npairs > (int64_t)blockIdx.x ? (npairs - blockIdx.x + G - 1) / G : 0;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_addr(&sm.tmem_base)),
@@ -1445,13 +1446,14 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05p(int64_t batch, c
         auto produce = [&](int64_t gp) {
             const int st = (int)(gp % VST);
             const int64_t pi = blockIdx.x + (gp / NCH) * G;
-            const int k0 = (int)(gp % NCH) * VKC, m0 = (int)(pi * 2 * PN);
-            const bool two = 2 * pi + 1 < batch;
+            const int k0 = (int)(gp % NCH) * VKC, m0 = (int)(pi * HN);
+            const int64_t left = batch - NPER * pi;
+            const int present = left < NPER ? (int)left : NPER;
             const unsigned fb = sm_addr(&sm.full[st]);
-            // A and B planes: always 2 x 2 x 2 KB (TMA zero-fills a missing second
-            // instance); A's columns: 2 KB per instance present
+            // A and B planes: always 2 x 2 x 2 KB (TMA zero-fills missing
+            // instances); A's columns: PN * 8 floats per instance present
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
-                         "r"(2u * HN * VKC * 4u + (two ? 2u : 1u) * PN * VKC * 4u)
+                         "r"(2u * HN * VKC * 4u + (unsigned)present * PN * VKC * 4u)
                          : "memory");
 #pragma unroll
             for (int kc = 0; kc < 2; ++kc) {
@@ -1466,10 +1468,10 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05p(int64_t batch, c
                     "l"(&tmB), "r"(k0 + 4 * kc), "r"(m0), "r"(fb)
                     : "memory");
             }
-            for (int q = 0; q < (two ? 2 : 1); ++q)
+            for (int q = 0; q < present; ++q)
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                                  sm_addr(&sm.sac[st][q * PN * VKC])),
-                             "l"(A + (2 * pi + q) * nn + (int64_t)k0 * PN), "r"((unsigned)(PN * VKC * 4)), "r"(fb)
+                             "l"(A + (NPER * pi + q) * nn + (int64_t)k0 * PN), "r"((unsigned)(PN * VKC * 4)), "r"(fb)
                              : "memory");
         };
         if (t == 0)
@@ -1499,8 +1501,8 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05p(int64_t batch, c
                 lv.w = vb.w - __uint_as_float(__float_as_uint(vb.w) & 0xffffe000u);
                 *reinterpret_cast<float4 *>(&sm.lo[lb][0][o]) = la;
                 *reinterpret_cast<float4 *>(&sm.lo[lb][1][o]) = lv;
-                // trace terms of instance 2p + (t >> 6), i = t & 63: B(k, i) * A(i, k)
-                const float *ac = &sm.sac[st][(t >> 6) * PN * VKC + (4 * q) * PN + (t & 63)];
+                // trace terms of instance NPER*p + t / PN, i = t % PN: B(k, i) * A(i, k)
+                const float *ac = &sm.sac[st][(t / PN) * PN * VKC + (4 * q) * PN + (t % PN)];
                 tr = fmaf(ac[0], vb.x, tr);
                 tr = fmaf(ac[PN], vb.y, tr);
                 tr = fmaf(ac[2 * PN], vb.z, tr);
@@ -1526,16 +1528,20 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_tc05p(int64_t batch, c
                 if (lane == 0) sm.red[warp] = tr;
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 const int64_t pj = blockIdx.x + j * G;
-                if (t == 0) S[2 * pj] = radd(sm.red[0], sm.red[1]);
-                if (t == 64 && 2 * pj + 1 < batch) S[2 * pj + 1] = radd(sm.red[2], sm.red[3]);
+                if (t % PN == 0 && NPER * pj + t / PN < batch) {
+                    const int w0 = (t / PN) * WPI;
+                    float sum = sm.red[w0];
+                    if (WPI == 2) sum = radd(sum, sm.red[w0 + 1]);
+                    S[NPER * pj + t / PN] = sum;
+                }
                 tr = 0.f;
             }
         }
     } else {
-        const int w4 = warp - 4, half = w4 >> 1, m = 32 * (w4 & 1) + lane;  // TMEM lane 32*w4 + lane
+        const int w4 = warp - 4, half = w4 / WPI, m = 32 * (w4 % WPI) + lane;  // TMEM lane 32*w4 + lane
         for (int64_t j = 0; j < J; ++j) {
             const int ab = (int)(j & 1);
-            const int64_t b = 2 * (blockIdx.x + j * G) + half;  // this warp's instance of the pair
+            const int64_t b = NPER * (blockIdx.x + j * G) + half;  // this warp's instance of the group
             mbar_wait(&sm.acc_full[ab], (unsigned)((j >> 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;");
             const bool live = b < batch;
@@ -1723,13 +1729,13 @@ static bool planes_tensor_map(CUtensorMap *tm, const float *base, int64_t batch)
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// n = 64 pairs: 2D view with 64-row columns; box 4 rows x 128 columns = one
-// 16-byte K piece of both instances of a pair
-static bool pair_planes_tensor_map(CUtensorMap *tm, const float *base, int64_t batch) {
+// n = PN (64 / 32): 2D view with PN-row columns; box 4 rows x 128 columns =
+// one 16-byte K piece of all 128 / PN instances of a group
+static bool group_planes_tensor_map(CUtensorMap *tm, const float *base, int64_t batch, int pn) {
     auto enc = tensor_map_encoder();
     if (!enc) return false;
-    cuuint64_t dims[2] = {64, (cuuint64_t)(batch * 64)};
-    cuuint64_t strides[1] = {64 * sizeof(float)};
+    cuuint64_t dims[2] = {(cuuint64_t)pn, (cuuint64_t)(batch * pn)};
+    cuuint64_t strides[1] = {(cuuint64_t)pn * sizeof(float)};
     cuuint32_t box[2] = {4, 128};
     cuuint32_t es[2] = {1, 1};
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, es,
@@ -1737,12 +1743,14 @@ static bool pair_planes_tensor_map(CUtensorMap *tm, const float *base, int64_t b
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int PN>
 int launch_tc05p(int64_t batch, const float *a, const float *b, const float *c, const float *d, float *e, float *s,
                  cudaStream_t st) {
     CUtensorMap ta, tb;
-    if (batch * 64 > 0x7fffffff || !pair_planes_tensor_map(&ta, a, batch) || !pair_planes_tensor_map(&tb, b, batch))
+    if (batch * PN > 0x7fffffff || !group_planes_tensor_map(&ta, a, batch, PN) ||
+        !group_planes_tensor_map(&tb, b, batch, PN))
         return 1;
-    auto kern = atb_schur_trace_tc05p;
+    auto kern = atb_schur_trace_tc05p<PN>;
     const size_t smem = sizeof(SmemTc05T) + 1024;
     static int grid = 0;
     if (!grid) {
@@ -1750,8 +1758,8 @@ int launch_tc05p(int64_t batch, const float *a, const float *b, const float *c, 
         LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         grid = 2 * num_sms();  // as launch_tc05t
     }
-    const int64_t np = (batch + 1) / 2;
-    const int64_t g = np < grid ? np : grid;
+    const int64_t ng = (batch + HN / PN - 1) / (HN / PN);
+    const int64_t g = ng < grid ? ng : grid;
     kern<<<(unsigned)g, 256, smem, st>>>(batch, a, c, d, e, s, ta, tb);
     LM_LAUNCHED(1);
     return 0;
@@ -1862,7 +1870,14 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
     if constexpr (sizeof(T) == 4) {
         static const int p64 = getenv("LM_5A_TC05P") ? atoi(getenv("LM_5A_TC05P")) : 1;
         if (aligned && n == 64 && p64) {
-            const int rc = launch_tc05p(batch, a, b, c, d, e, s, st);
+            const int rc = launch_tc05p<64>(batch, a, b, c, d, e, s, st);
+            if (rc <= 0) return rc;
+        }
+        // n = 32 in groups of four measured no faster than the FFMA kernel
+        // (0.41 vs 0.40 ms): off by default
+        static const int q32 = getenv("LM_5A_TC05Q") ? atoi(getenv("LM_5A_TC05Q")) : 0;
+        if (aligned && n == 32 && q32) {
+            const int rc = launch_tc05p<32>(batch, a, b, c, d, e, s, st);
             if (rc <= 0) return rc;
         }
     }

@@ -20,8 +20,10 @@ import numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 from paper_2502_03000_b200.batch import atb_schur_trace, stack_fortran
 dt = torch.float64 if sys.argv[2] == "f64" else torch.float32
+import os
 rng = np.random.default_rng(11)
-bt, n = 400, 128
+n = int(os.environ.get("LM_5A_N", "128"))
+bt = 400 if n == 128 else 401
 ops = [rng.uniform(-1, 1, (bt, n, n)) for _ in range(4)]
 E, s = atb_schur_trace(*(stack_fortran(o, dtype=dt) for o in ops))
 idx = [0, 1, 147, 148, 296, 299, 399]
@@ -55,4 +57,14 @@ def test_f64_variants_agree(variant):
 def test_f32_variants_agree(variant):
     ref = run({}, "f32")
     got = run(variant, "f32")
+    assert close(got["E"], ref["E"], 1e-5) and close(got["s"], ref["s"], 1e-5)
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_f32_grouped_small_sizes_agree(n):
+    """n = 64 in pairs (default) and n = 32 in groups of four (LM_5A_TC05Q=1)
+    per 128 x 128 tcgen05 tile vs the FFMA kernel (LM_5A_TC05P=0), 401
+    instances (a partial last group)."""
+    ref = run({"LM_5A_TC05P": "0", "LM_5A_N": str(n)}, "f32")
+    got = run({"LM_5A_TC05Q": "1", "LM_5A_N": str(n)}, "f32")
     assert close(got["E"], ref["E"], 1e-5) and close(got["s"], ref["s"], 1e-5)
