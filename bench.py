@@ -2,27 +2,39 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-Workloads are the BASELINE.json configs; the default,
-C=2, is configs[1]: trace(A*B), diagmat(v)*B and A*diagmat(v) on float64
-4096x4096 A, B and a length-4096 v, entries U(-1,1) (seeded synthetic
-data, no dataset is involved).  A *step* is one evaluation of the
-config's expressions through the public API.
+Workloads are the BASELINE.json configs.  The default,
+C=5a, is the largest single-GPU configuration (configs[4]): 262144
+independent instances of E = A.t()*B + C % D and s = trace(A*B), float64,
+square sizes drawn uniformly from {32, 64, 128}, U(-1,1) entries (75 GB of
+operands resident in HBM).  Inputs are seeded synthetic data, generated on
+the device bit-identical to the numpy scheme of SURVEY.md 8(d)
+(paper_2502_03000_b200/datagen.py); no dataset is involved.  A *step* is
+one evaluation of the config's expressions through the public API.
 
+verified     before anything is timed, a sample of the step's own outputs
+             is compared with the oracle (oracle/, the reference loops
+             restated in C) at the north-star tolerance -- the reference
+             harness verifies before it times (lazymat/bench.py:184-190).
 value        algorithmic bytes (or flops) per step x steps, all ranks, / the
              max-over-ranks device time of K steps (CUDA events around CUDA-
              graph replays of the compiled plans; inputs resident in HBM).
-e2e          the same metric through evaluate() from pinned HOST buffers:
-             H2D of the inputs and D2H of every result inside the timed
-             region (rewrite + device structure scans included).
-roofline     the dominant kernel's algorithmic bytes / its CUDA-event
-             duration vs the measured HBM copy peak (MEASURED_PEAKS.json).
-cpu_baseline the reference's loops restated in C (oracle/, single thread,
-             same inputs) on a bounded sample -- a reported baseline only.
---impl reference  times that CPU restatement as the reference arm.
+e2e          the same metric through the public API from pinned HOST
+             buffers: H2D of the inputs and D2H of every result inside the
+             timed region.
+roofline     the dominant kernel's algorithmic work / its CUDA-event
+             duration vs the measured HBM copy peak (MEASURED_PEAKS.json) or
+             the measured FP64 peak (profiles/fp64_peak.json).
+cpu_baseline the reference's loops restated in C (oracle/) on one core of
+             the host, on a bounded sample; batched configs add an all-core
+             process pool (`all_cores`).
+--impl reference  times that CPU restatement as the reference arm, with
+             every host core for the batched configs (independent instances).
 
-Multi-GPU: these configs do not shard (replicas only) --
-every rank runs the same workload independently; value = total work of
-all ranks / max rank time.
+Multi-GPU (`--gpus N`; without torchrun this script launches N ranks
+itself): configs 4b and 5a partition the FIXED batch into contiguous
+instance ranges balanced by realised n^3 (strong scaling, no collective);
+5b row-shards the 32768^2 matrices (one NCCL scalar all-reduce); the
+single-problem configs 1-4a run one replica per rank (weak scaling).
 """
 
 from __future__ import annotations
@@ -31,7 +43,9 @@ import argparse
 import json
 import os
 import pathlib
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -43,13 +57,14 @@ sys.path.insert(0, str(ROOT))
 
 BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
 METRIC = BASELINE["metric"]
+DEFAULT_CONFIG = "5a"
 
 
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback"
 
 
@@ -57,6 +72,35 @@ def seeded(config: int, k: int, shape, seed: int = 42) -> np.ndarray:
     """Operand k of config c: default_rng(1000003*seed + 101*c + k).uniform(-1,1), F-order."""
     rng = np.random.default_rng(1000003 * seed + 101 * config + k)
     return np.asfortranarray(rng.uniform(-1.0, 1.0, shape))
+
+
+def _np(x):
+    """Host numpy copy of a step output (DenseMatrix, tensor or float)."""
+    if hasattr(x, "to_numpy"):
+        return x.to_numpy()
+    if hasattr(x, "detach"):
+        return x.detach().cpu().numpy()
+    return np.asarray(x)
+
+
+def _bitwise(a, b) -> bool:
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.int64) if a.dtype == np.float64 else a,
+                                                 b.view(np.int64) if b.dtype == np.float64 else b)
+
+
+def _normwise(a, b) -> float:
+    """max|a - b| / max|b| (lazymat/bench.py:139-143)."""
+    a, b = np.asarray(a, dtype=np.float64), np.asarray(b, dtype=np.float64)
+    den = np.max(np.abs(b)) if b.size else 0.0
+    return float(np.max(np.abs(a - b)) / den) if den > 0 else float(np.max(np.abs(a - b), initial=0.0))
+
+
+def _host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 # ---------------------------------------------------------------------------------------
@@ -117,6 +161,61 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
+# all-core CPU pool (batched configs: independent instances)
+# ---------------------------------------------------------------------------------------
+
+def _pool_worker(config, wid, conn):
+    from oracle import lm_oracle as O
+    wl = WORKLOADS[config]()
+    state = wl.pool_prepare(O, wid)
+    conn.send("ready")
+    while True:
+        rounds = conn.recv()
+        if rounds is None:
+            break
+        for _ in range(rounds):
+            wl.pool_round(O, state)
+        conn.send("done")
+    conn.close()
+
+
+class CpuPool:
+    """One process per host core, each running the oracle on its own
+    instances of the workload (generated in the worker, untimed).  A step
+    is one round on every worker; its time is the parent's wall clock from
+    the first send to the last reply."""
+
+    def __init__(self, config: str, workers: int):
+        import multiprocessing as mp
+        ctx = mp.get_context("fork")  # created before any CUDA context exists in this process
+        self.workers = workers
+        self.procs, self.conns = [], []
+        for w in range(workers):
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_pool_worker, args=(config, w, b), daemon=True)
+            p.start()
+            self.procs.append(p)
+            self.conns.append(a)
+        for c in self.conns:
+            if c.recv() != "ready":
+                raise RuntimeError("pool worker failed")
+
+    def step(self, rounds: int = 1) -> float:
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(rounds)
+        for c in self.conns:
+            c.recv()
+        return time.perf_counter() - t0
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(timeout=10)
+
+
+# ---------------------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------------------
 
@@ -129,6 +228,8 @@ class Workload:
     graphable = True  # the step has no host synchronisation -> CUDA graph replay
     workload = ""
     dtype = "f64"
+    scaling = "weak"  # replicas per rank unless the workload partitions
+    pool = False  # independent instances: an all-core CPU pool is meaningful
 
     def cpu_work_per_step(self):
         return self.work_per_step()
@@ -139,7 +240,7 @@ class Workload:
     def expressions(self, lm, mats) -> list:
         raise NotImplementedError
 
-    def work_per_step(self) -> float:  # bytes (GB/s) or flops (TFLOP/s)
+    def work_per_step(self) -> float:  # bytes (GB/s) or flops (TFLOP/s), ALL ranks
         raise NotImplementedError
 
     def kernels_for_roofline(self, lm, mats):
@@ -149,8 +250,29 @@ class Workload:
     def cpu_step(self, O, host) -> None:
         raise NotImplementedError
 
+    def verify(self, lm, ctx, host, outs, O):
+        """(ok, details): the step's outputs vs the oracle."""
+        return None, {"note": "no verification defined"}
+
     def scale(self) -> float:
         return 1e9 if self.unit == "GB/s" else 1e12
+
+
+# The f32 n=128 batched kernel runs A.T*B as 3xTF32 on mma.sync.m16n8k8.tf32:
+# 275.2 TF/s measured (tools/tf32_probe.cu, profiles/r01_tf32_probe.txt),
+# three MMAs per product -> an effective f32 ceiling of a third of that.
+TF32_MMA_TFLOPS = 275.2
+
+
+def _tf32x3_peak():
+    return TF32_MMA_TFLOPS / 3.0, "3xTF32 effective (legacy mma.sync tf32 275.2 TF/s measured / 3)"
+
+
+def _fp64_peak():
+    p = ROOT / "profiles" / "fp64_peak.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["tflops"]), "measured (tools/fp64_probe.cu)"
+    return 37.0, "fallback"
 
 
 class Config2(Workload):
@@ -224,6 +346,18 @@ class Config2(Workload):
         O.diag_scale(np.ascontiguousarray(h["v"][:, 0]), h["B"], "left", out)
         O.diag_scale(np.ascontiguousarray(h["v"][:, 0]), h["A"], "right", out)
 
+    def verify(self, lm, ctx, h, outs, O):
+        t = float(_np(outs[0]).ravel()[0])
+        tref = O.trace_of_product(h["A"], h["B"])
+        v = np.ascontiguousarray(h["v"][:, 0])
+        left, right = (np.empty(h["A"].shape, order="F") for _ in range(2))
+        O.diag_scale(v, h["B"], "left", left)
+        O.diag_scale(v, h["A"], "right", right)
+        rel = abs(t - tref) / abs(tref)
+        ok = rel <= 1e-12 and _bitwise(_np(outs[1]), left) and _bitwise(_np(outs[2]), right)
+        return ok, {"trace_rel_err": rel, "trace_tol": 1e-12, "diag_scale": "bitwise vs oracle, both sides",
+                    "size": "full 4096^2"}
+
 
 class Config1(Workload):
     config = 1
@@ -283,22 +417,16 @@ class Config1(Workload):
         out = np.empty((self.N, self.N), order="F")
         O.program(ops.numpy(), args.numpy(), [2.0, 1.0], [h["A"], h["B"], h["C"]], out)
 
+    def verify(self, lm, ctx, h, outs, O):
+        ref = np.empty((self.N, self.N), order="F")
+        self.cpu_step_into(O, h, ref)
+        return _bitwise(_np(outs[0]), ref), {"D": "bitwise vs oracle program (per-node IEEE order)",
+                                             "size": "full 4096^2"}
 
-# The f32 n=128 batched kernel runs A.T*B as 3xTF32 on mma.sync.m16n8k8.tf32:
-# 275.2 TF/s measured (tools/tf32_probe.cu, profiles/r01_tf32_probe.txt),
-# three MMAs per product -> an effective f32 ceiling of a third of that.
-TF32_MMA_TFLOPS = 275.2
-
-
-def _tf32x3_peak():
-    return TF32_MMA_TFLOPS / 3.0, "3xTF32 effective (legacy mma.sync tf32 275.2 TF/s measured / 3)"
-
-
-def _fp64_peak():
-    p = ROOT / "profiles" / "fp64_peak.json"
-    if p.exists():
-        return float(json.loads(p.read_text())["tflops"]), "measured (tools/fp64_probe.cu)"
-    return 37.0, "fallback"
+    def cpu_step_into(self, O, h, out):
+        from paper_2502_03000_b200.kernels import parse_program
+        ops, args, *_ = parse_program("x0 c0 * x1 x2 * + x0 x1 abs c1 + / -")
+        O.program(ops.numpy(), args.numpy(), [2.0, 1.0], [h["A"], h["B"], h["C"]], out)
 
 
 class Config3a(Workload):
@@ -333,6 +461,15 @@ class Config3a(Workload):
         O.gemm(h["B"], t1, t2)
         O.gemm(h["A"], t2, t3)
 
+    def verify(self, lm, ctx, h, outs, O):
+        n = self.N
+        t1, t2, t3 = (np.zeros((n, 1), order="F") for _ in range(3))
+        O.gemm(h["C"], h["v"], t1)
+        O.gemm(h["B"], t1, t2)
+        O.gemm(h["A"], t2, t3)
+        err = _normwise(_np(outs[0]), t3)
+        return err <= 1e-12, {"normwise_err": err, "tol": 1e-12, "size": "full 4096^2 chain"}
+
 
 class Config3b(Workload):
     config = "3b"
@@ -361,6 +498,14 @@ class Config3b(Workload):
         O.gemm(h["Y"], h["Z"], yz)
         out = np.zeros((8000, 100), order="F")
         O.gemm(h["X"], yz, out)
+
+    def verify(self, lm, ctx, h, outs, O):
+        yz = np.zeros((100, 100), order="F")
+        O.gemm(h["Y"], h["Z"], yz)
+        ref = np.zeros((8000, 100), order="F")
+        O.gemm(h["X"], yz, ref)
+        err = _normwise(_np(outs[0]), ref)
+        return err <= 1e-12, {"normwise_err": err, "tol": 1e-12, "size": "full 8000x100 chain"}
 
 
 class Config3c(Workload):
@@ -398,6 +543,26 @@ class Config3c(Workload):
     def cpu_work_per_step(self):
         return self.K * (self.K + 1) * self.cpu_sample_k
 
+    def verify(self, lm, ctx, h, outs, O):
+        """16 sampled 64x64 output tiles (diagonal, edge, interior, both
+        triangles) vs the oracle's gemm on the matching column slices of A,
+        over all 16384 inner terms; plus the whole device output bitwise
+        symmetric."""
+        import torch
+        out = outs[0].data if hasattr(outs[0], "data") else outs[0]
+        sym = bool(torch.equal(out, out.t()))
+        S = out.cpu().numpy()
+        A = h["A"]
+        starts = [0, 64, 960, 1024, 1984]
+        tiles = [(i, j) for i in starts for j in starts if abs(i - j) <= 1024][:16]
+        worst = 0.0
+        for (i0, j0) in tiles:
+            ref = np.zeros((64, 64), order="F")
+            O.gemm(A[:, i0:i0 + 64].T, A[:, j0:j0 + 64], ref)
+            worst = max(worst, _normwise(S[i0:i0 + 64, j0:j0 + 64], ref))
+        return sym and worst <= 1e-12, {"tiles": len(tiles), "tile_normwise_err_max": worst, "tol": 1e-12,
+                                        "bitwise_symmetric": sym, "size": "full 16384x2048"}
+
 
 class Config4a(Workload):
     config = "4a"
@@ -406,7 +571,7 @@ class Config4a(Workload):
     graphable = False
     N, NRHS = 8192, 64
     workload = ("inverse(A)*b -> LU solve (R9), float64 A = U(-1,1) + 8192*I (data leaf), b 8192x64; "
-                "exact reference operation order (bit-identical pivots and values)")
+                "exact reference operation order")
 
     def host_inputs(self):
         n = self.N
@@ -458,21 +623,55 @@ class Config4a(Workload):
         n, k = self.cpu_n, self.NRHS
         return 2 * n * n * n // 3 + 2 * n * n * k
 
+    def verify(self, lm, ctx, h, outs, O):
+        X = _np(outs[0])
+        A, B = h["A"], h["b"]
+        r = A @ X - B
+        res = np.abs(r).sum(axis=1).max() / (np.abs(A).sum(axis=1).max() * np.abs(X).sum(axis=1).max() +
+                                             np.abs(B).sum(axis=1).max())
+        return res <= 1e-10, {"scaled_residual": float(res), "tol": 1e-10, "size": "full 8192^2, 64 rhs",
+                              "norm": "inf-norm, lazymat tests/test_kernels.py:169-179 form"}
+
+
+def _ws():
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+
+
+def _spread(first: int, count: int, k: int) -> list:
+    """k local indices spread over [0, count): both ends and the tail included."""
+    if count <= k:
+        return list(range(count))
+    idx = set(np.linspace(0, count - 1, k - 4).round().astype(int).tolist())
+    idx.update([0, 1, count - 2, count - 1])
+    return sorted(idx)
+
 
 class Config4b(Workload):
     config = "4b"
     unit = "GB/s"
     graphable = False
+    scaling = "strong"
+    pool = True
     N, BATCH = 64, 4096
     workload = ("4096 independent inverse(A_i)*b_i, A_i = U(-1,1) + 64*I (64x64), b_i 64x1: batched structure "
-                "scan + in-shared-memory LU in the reference's exact order")
+                "scan + in-register LU in the reference's exact order; instances partitioned across ranks")
+    POOL_SYSTEMS = 64  # per worker per round
 
-    def host_inputs(self):
+    def __init__(self):
+        from paper_2502_03000_b200.shard import partition_by_cost
+        self.ws, self.rank = _ws()
+        self.lo, self.hi = partition_by_cost(np.ones(self.BATCH), self.ws)[self.rank]
+
+    def _full(self, seed_k=7):
         n, bt = self.N, self.BATCH
-        rng = np.random.default_rng(1000003 * 42 + 101 * 4 + 7)
+        rng = np.random.default_rng(1000003 * 42 + 101 * 4 + seed_k)
         a = rng.uniform(-1.0, 1.0, (bt, n, n)) + n * np.eye(n)[None]
         b = rng.uniform(-1.0, 1.0, (bt, n, 1))
-        return {"A": a, "b": b}
+        return a, b
+
+    def host_inputs(self):
+        a, b = self._full()
+        return {"A": a[self.lo:self.hi], "b": b[self.lo:self.hi]}
 
     def setup(self, lm, h):
         from paper_2502_03000_b200.batch import stack_fortran
@@ -482,65 +681,106 @@ class Config4b(Workload):
         from paper_2502_03000_b200.batch import solve_batched
         return lambda: [solve_batched(ctx["A"], ctx["b"]).x]
 
+    def verify(self, lm, ctx, h, outs, O):
+        x = outs[0]
+        idx = _spread(0, x.shape[0], 64)
+        xs = x[idx].cpu().numpy()
+        bad = []
+        for t, i in enumerate(idx):
+            rc, lu, piv = O.lu_factor(np.asfortranarray(h["A"][i]))
+            xr = np.array(h["b"][i], order="F")
+            O.lu_solve(lu, piv, xr)
+            if rc != 0 or not _bitwise(xs[t], xr):
+                bad.append(int(i) + self.lo)
+        return not bad, {"instances_checked": len(idx), "criterion": "x bitwise vs oracle lu_factor+lu_solve",
+                         "mismatches": bad[:8]}
+
     def e2e_fn(self, lm, h):
         import torch
         from paper_2502_03000_b200.batch import solve_batched
         pa = torch.from_numpy(np.ascontiguousarray(np.transpose(h["A"], (0, 2, 1)))).pin_memory()
         pb = torch.from_numpy(np.ascontiguousarray(h["b"])).pin_memory()
         px = torch.empty_like(pb).pin_memory()
-
-        K = 4  # instance chunks: chunk k is solved while chunks > k are still uploading
-        bt = self.BATCH
-        bk = bt // K
+        bt = pa.shape[0]
+        K = 4 if bt >= 4 else 1  # instance chunks: chunk k is solved while chunks > k are still uploading
+        bounds = [(k * bt // K, (k + 1) * bt // K) for k in range(K)]
         h2d = torch.cuda.Stream()
 
         def run():
             chunks = []
             h2d.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(h2d):
-                for k in range(K):
-                    A = pa[k * bk:(k + 1) * bk].cuda(non_blocking=True).transpose(1, 2)
-                    b = pb[k * bk:(k + 1) * bk].cuda(non_blocking=True)
+                for lo, hi in bounds:
+                    A = pa[lo:hi].cuda(non_blocking=True).transpose(1, 2)
+                    b = pb[lo:hi].cuda(non_blocking=True)
                     ev = torch.cuda.Event()
                     ev.record(h2d)
                     chunks.append((A, b, ev))
-            for k, (A, b, ev) in enumerate(chunks):
+            for (lo, hi), (A, b, ev) in zip(bounds, chunks):
                 torch.cuda.current_stream().wait_event(ev)
+                A.record_stream(torch.cuda.current_stream())
+                b.record_stream(torch.cuda.current_stream())
                 x = solve_batched(A, b).x
-                px[k * bk:(k + 1) * bk].copy_(x, non_blocking=True)
+                px[lo:hi].copy_(x, non_blocking=True)
             torch.cuda.synchronize()
             return [px]
         return run, pa.numel() * 8 + pb.numel() * 8, px.numel() * 8
 
     def work_per_step(self):
         n, bt = self.N, self.BATCH
-        return bt * (n * n * 8 + 2 * n * 8)  # A read once, b read, x written
+        return bt * (n * n * 8 + 2 * n * 8)  # A read once, b read, x written (whole batch, all ranks)
+
+    def rank_work(self):
+        n = self.N
+        return (self.hi - self.lo) * (n * n * 8 + 2 * n * 8)
 
     exact_fp64 = True
 
     def kernels_for_roofline(self, lm, ctx):
         import torch
         from paper_2502_03000_b200 import _native as N
-        n, bt = self.N, self.BATCH
         A = ctx["A"]
+        bt, n = A.shape[0], self.N
         x = torch.empty((bt, 1, n), dtype=torch.float64, device=A.device).transpose(1, 2)
         x.copy_(ctx["b"])
         info = torch.empty(bt, dtype=torch.int32, device=A.device)
 
         def solve():  # in place: repeated solves do the same work
             N.call("lm_lu_solve_batched", 0, n, bt, A.data_ptr(), x.data_ptr(), None, None, info.data_ptr())
-        return [("lu_solve_batched", self.work_per_step(), solve, self.flops_per_step())]
+        return [("lu_solve_batched", bt * (n * n * 8 + 2 * n * 8), solve, bt * (2 * n ** 3 // 3 + 2 * n * n))]
 
     def flops_per_step(self):
         n, bt = self.N, self.BATCH
         return bt * (2 * n * n * n // 3 + 2 * n * n)
 
+    cpu_sample_desc = "the rank's systems, oracle lu_factor + lu_solve each"
+
     def cpu_step(self, O, h):
-        n = self.N
-        for i in range(self.BATCH):
+        for i in range(h["A"].shape[0]):
             rc, lu, piv = O.lu_factor(np.asfortranarray(h["A"][i]))
             x = np.array(h["b"][i], order="F")
             O.lu_solve(lu, piv, x)
+
+    def cpu_work_per_step(self):
+        return self.rank_work()
+
+    # all-core pool: each worker solves its own 64 systems per round
+    def pool_prepare(self, O, wid):
+        n = self.N
+        rng = np.random.default_rng([1000003 * 42 + 101 * 4 + 7, 1000 + wid])
+        A = [np.asfortranarray(rng.uniform(-1, 1, (n, n)) + n * np.eye(n)) for _ in range(self.POOL_SYSTEMS)]
+        b = [np.asfortranarray(rng.uniform(-1, 1, (n, 1))) for _ in range(self.POOL_SYSTEMS)]
+        return A, b
+
+    def pool_round(self, O, state):
+        for A, b in zip(*state):
+            rc, lu, piv = O.lu_factor(A)
+            x = np.array(b, order="F")
+            O.lu_solve(lu, piv, x)
+
+    def pool_work_round(self):
+        n = self.N
+        return self.POOL_SYSTEMS * (n * n * 8 + 2 * n * 8)
 
 
 class Config5a(Workload):
@@ -550,104 +790,201 @@ class Config5a(Workload):
     BATCH = 262144
     SIZES = (32, 64, 128)
     dtype = "f64"
+    scaling = "strong"
+    pool = True
     workload = ("262144 independent E = A.t()*B + C % D and s = trace(A*B), square sizes drawn uniformly from "
-                "{32,64,128}, U(-1,1); one grouped kernel per size class")
-    e2e_sample = 4096  # instances per size class pushed through the API from host memory
+                "{32,64,128}, U(-1,1) float64; one grouped kernel per size class; instances partitioned across "
+                "ranks by realised n^3")
+    CPU_SAMPLE = {32: 96, 64: 48, 128: 16}  # single-core sample (and per pool worker per round: POOL_SAMPLE)
+    POOL_SAMPLE = {32: 24, 64: 12, 128: 4}
+    VERIFY_PER_CLASS = 256
+    e2e_per_class = 8192
 
-    def counts(self):
-        rng = np.random.default_rng(1000003 * 42 + 101 * 5 + 99)
-        sizes = rng.choice(self.SIZES, self.BATCH)
-        return {n: int((sizes == n).sum()) for n in self.SIZES}
+    def __init__(self):
+        from paper_2502_03000_b200.datagen import batch_sizes
+        from paper_2502_03000_b200.shard import class_ranges, partition_by_cost
+        self.ws, self.rank = _ws()
+        self.sizes = batch_sizes(self.BATCH, self.SIZES)
+        self.lo, self.hi = partition_by_cost(self.sizes.astype(np.float64) ** 3, self.ws)[self.rank]
+        self.ranges = class_ranges(self.sizes, self.lo, self.hi, self.SIZES)
 
     @property
     def width(self):
         return 8 if self.dtype == "f64" else 4
 
-    def work_per_step(self):
+    def counts(self):
+        return {n: int((self.sizes == n).sum()) for n in self.SIZES}
+
+    def _bytes(self, counts):
         w = self.width
-        return sum(c * (5 * n * n * w + w) for n, c in self.counts().items())
+        return sum(c * (5 * n * n * w + w) for n, c in counts.items())
+
+    def _flops(self, counts):
+        return sum(c * (2 * n ** 3 + 4 * n * n) for n, c in counts.items())
+
+    def work_per_step(self):  # the whole batch (all ranks)
+        return self._bytes(self.counts())
 
     def flops_per_step(self):
-        return sum(c * (2 * n ** 3 + 4 * n * n) for n, c in self.counts().items())
+        return self._flops(self.counts())
+
+    def rank_counts(self):
+        return {n: c for n, (f, c) in self.ranges.items()}
+
+    def _tdt(self):
+        import torch
+        return torch.float64 if self.dtype == "f64" else torch.float32
+
+    def _host_instance(self, k, n, idx):
+        from paper_2502_03000_b200.datagen import host_batch_instance
+        x = host_batch_instance(k, n, idx)
+        return x if self.dtype == "f64" else np.asfortranarray(x.astype(np.float32).astype(np.float64))
 
     def host_inputs(self):
-        # bounded CPU sample (the full batch is generated on the device)
-        rng = np.random.default_rng(1000003 * 42 + 101 * 5 + 1)
-        return {n: rng.uniform(-1, 1, (4, self.CPU_SAMPLE[n], n, n)) for n in self.SIZES}
-
-    CPU_SAMPLE = {32: 96, 64: 48, 128: 16}
-    cpu_sample_desc = "160 instances (96 of n=32, 48 of n=64, 16 of n=128), oracle gemm + program + trace each"
+        # bounded single-core CPU sample: the first CPU_SAMPLE[n] instances of each class
+        return {n: [[self._host_instance(k, n, i) for k in range(4)] for i in range(self.CPU_SAMPLE[n])]
+                for n in self.SIZES}
 
     def setup(self, lm, host):
-        import torch
         from paper_2502_03000_b200.batch import empty_batch
-        tdt = torch.float64 if self.dtype == "f64" else torch.float32
-        g = torch.Generator(device="cuda")
-        g.manual_seed(1000003 * 42 + 101 * 5)
+        from paper_2502_03000_b200.datagen import fill_batch_class
         ctx = {}
-        for n, c in self.counts().items():
-            ops = []
-            for _ in range(4):
-                t = empty_batch(c, n, n, tdt)
-                t.uniform_(-1.0, 1.0, generator=g)
-                ops.append(t)
-            ctx[n] = ops
+        for n, (first, count) in self.ranges.items():
+            ctx[n] = [fill_batch_class(empty_batch(count, n, n, self._tdt()), k, n, first) for k in range(4)]
         return ctx
 
     def step_fn(self, lm, ctx):
         from paper_2502_03000_b200.batch import atb_schur_trace
         return lambda: [atb_schur_trace(*ctx[n]) for n in self.SIZES]
 
+    def verify(self, lm, ctx, h, outs, O):
+        """VERIFY_PER_CLASS instances per size class, spread over the rank's
+        class range (both ends: the persistent loops' tail), inputs
+        regenerated on the host with numpy (so the device generator is
+        checked too), E normwise and s against the oracle."""
+        from paper_2502_03000_b200.kernels import parse_program
+        ops, args, *_ = parse_program("x0 x1 x2 * +")
+        tol = 1e-12 if self.dtype == "f64" else 1e-5
+        worst_e = worst_s = 0.0
+        checked, bad = 0, []
+        for ci, n in enumerate(self.SIZES):
+            first, count = self.ranges[n]
+            E, s = outs[ci]
+            idx = _spread(first, count, self.VERIFY_PER_CLASS)
+            Ed = E[idx].double().cpu().numpy()
+            sd = s[idx].double().cpu().numpy()
+            for t, i in enumerate(idx):
+                A, B, C, D = (self._host_instance(k, n, first + i) for k in range(4))
+                g = np.zeros((n, n), order="F")
+                O.gemm(A.T, B, g)
+                Er = np.zeros((n, n), order="F")
+                O.program(ops.numpy(), args.numpy(), [], [g, C, D], Er)
+                tr = O.trace_of_product(A, B)
+                ee = _normwise(Ed[t], Er)
+                se = abs(sd[t] - tr) / max(abs(tr), np.sum(np.abs(A * B.T)) * 1e-2)
+                worst_e, worst_s = max(worst_e, ee), max(worst_s, se)
+                if ee > tol or se > tol:
+                    bad.append((n, first + i))
+                checked += 1
+        return not bad, {"instances_checked": checked, "per_class": self.VERIFY_PER_CLASS,
+                         "E_normwise_err_max": worst_e, "s_rel_err_max": worst_s, "tol": tol,
+                         "inputs": "regenerated on the host with numpy (checks the device generator)",
+                         "mismatches": bad[:8]}
+
     def kernels_for_roofline(self, lm, ctx):
         from paper_2502_03000_b200.batch import atb_schur_trace
         out = []
-        for n, c in self.counts().items():
-            out.append((f"atb_schur_trace n={n}", c * (5 * n * n * self.width + self.width),
-                        lambda n=n: atb_schur_trace(*ctx[n]), c * (2 * n ** 3 + 4 * n * n)))
+        for n, c in self.rank_counts().items():
+            if c:
+                out.append((f"atb_schur_trace n={n}", self._bytes({n: c}),
+                            lambda n=n: atb_schur_trace(*ctx[n]), self._flops({n: c})))
         return out
+
+    cpu_sample_desc = "160 instances (96 of n=32, 48 of n=64, 16 of n=128), oracle gemm + program + trace each"
+
+    def _cpu_instance(self, O, n, A, B, C, D, ops, args):
+        g = np.zeros((n, n), order="F")
+        O.gemm(A.T, B, g)
+        E = np.zeros((n, n), order="F")
+        O.program(ops, args, [], [g, C, D], E)
+        O.trace_of_product(A, B)
 
     def cpu_step(self, O, h):
         from paper_2502_03000_b200.kernels import parse_program
         ops, args, *_ = parse_program("x0 x1 x2 * +")
+        ops, args = ops.numpy(), args.numpy()
         for n in self.SIZES:
-            x = h[n]
-            for i in range(x.shape[1]):
-                A, B, C, D = (np.asfortranarray(x[k, i]) for k in range(4))
-                g = np.zeros((n, n), order="F")
-                O.gemm(A.T, B, g)
-                E = np.zeros((n, n), order="F")
-                O.program(ops.numpy(), args.numpy(), [], [g, C, D], E)
-                O.trace_of_product(A, B)
+            for A, B, C, D in h[n]:
+                self._cpu_instance(O, n, A, B, C, D, ops, args)
 
     def cpu_work_per_step(self):
-        w = 8
-        return sum(self.CPU_SAMPLE[n] * (5 * n * n * w + w) for n in self.SIZES)
+        return self._bytes(self.CPU_SAMPLE)
 
-    def e2e_fn(self, lm, h):
-        import torch
-        from paper_2502_03000_b200.batch import atb_schur_trace
-        tdt = torch.float64 if self.dtype == "f64" else torch.float32
-        k = self.e2e_sample
-        pinned = {n: [torch.empty((k, n, n), dtype=tdt).uniform_(-1, 1).pin_memory() for _ in range(4)]
-                  for n in self.SIZES}
-        outs = {n: (torch.empty((k, n, n), dtype=tdt).pin_memory(), torch.empty(k, dtype=tdt).pin_memory())
+    def pool_prepare(self, O, wid):
+        from paper_2502_03000_b200.datagen import host_matrix
+        from paper_2502_03000_b200.kernels import parse_program
+        ops, args, *_ = parse_program("x0 x1 x2 * +")
+        rng_seed = [1000003 * 42 + 101 * 5 + 77, wid]
+        inst = {n: [[host_matrix(rng_seed + [n, i, k], n, n) for k in range(4)] for i in range(self.POOL_SAMPLE[n])]
                 for n in self.SIZES}
+        return inst, ops.numpy(), args.numpy()
+
+    def pool_round(self, O, state):
+        inst, ops, args = state
+        for n in self.SIZES:
+            for A, B, C, D in inst[n]:
+                self._cpu_instance(O, n, A, B, C, D, ops, args)
+
+    def pool_work_round(self):
+        return self._bytes(self.POOL_SAMPLE)
+
+    def e2e_fn(self, lm, ctx):
+        """Through the batch API from pinned host buffers, pipelined over
+        chunks of 1024 instances: chunk j's inputs upload on one copy stream
+        while chunk j-1 computes and chunk j-2's results download on
+        another (PCIe carries both directions at once).  A bounded sample
+        (e2e_per_class instances of each class, copied from the resident
+        seeded batch) keeps the pinned host footprint to a few GB."""
+        import torch
+        from paper_2502_03000_b200.batch import atb_schur_trace, empty_batch
+        tdt, w = self._tdt(), self.width
+        k = {n: min(self.e2e_per_class, c) for n, c in self.rank_counts().items()}
+        host_in, dev_in, host_out, dev_out = {}, {}, {}, {}
+        for n in self.SIZES:
+            if not k[n]:
+                continue
+            host_in[n] = [torch.empty((k[n], n, n), dtype=tdt).pin_memory().transpose(1, 2) for _ in range(4)]
+            for t, src in zip(host_in[n], ctx[n]):
+                t.copy_(src[:k[n]])
+            dev_in[n] = [empty_batch(k[n], n, n, tdt) for _ in range(4)]
+            dev_out[n] = (empty_batch(k[n], n, n, tdt), torch.empty(k[n], dtype=tdt, device="cuda"))
+            host_out[n] = (torch.empty((k[n], n, n), dtype=tdt).pin_memory().transpose(1, 2),
+                           torch.empty(k[n], dtype=tdt).pin_memory())
+        h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+        CH = 1024
+        comp = torch.cuda.current_stream()
 
         def run():
-            res = []
-            for n in self.SIZES:
-                dev = [p.cuda(non_blocking=True).transpose(1, 2) for p in pinned[n]]
-                E, s = atb_schur_trace(*dev)
-                outs[n][0].copy_(E.transpose(1, 2))
-                outs[n][1].copy_(s)
-                res += list(outs[n])
+            h2d.wait_stream(comp)
+            d2h.wait_stream(comp)
+            for n in host_in:
+                for lo in range(0, k[n], CH):
+                    hi = min(k[n], lo + CH)
+                    with torch.cuda.stream(h2d):
+                        for t, hsrc in zip(dev_in[n], host_in[n]):
+                            t[lo:hi].copy_(hsrc[lo:hi], non_blocking=True)
+                    comp.wait_stream(h2d)
+                    E, s = dev_out[n]
+                    atb_schur_trace(*(t[lo:hi] for t in dev_in[n]), out=(E[lo:hi], s[lo:hi]))
+                    d2h.wait_stream(comp)
+                    with torch.cuda.stream(d2h):
+                        host_out[n][0][lo:hi].copy_(E[lo:hi], non_blocking=True)
+                        host_out[n][1][lo:hi].copy_(s[lo:hi], non_blocking=True)
             torch.cuda.synchronize()
-            return res
-        w = self.width
-        h2d = sum(4 * k * n * n * w for n in self.SIZES)
-        d2h = sum(k * (n * n + 1) * w for n in self.SIZES)
-        self.e2e_work = sum(k * (5 * n * n * w + w) for n in self.SIZES)
-        return run, h2d, d2h
+            return [v for n in host_out for v in host_out[n]]
+        self.e2e_work = self._bytes(k)
+        self.e2e_sample = f"{self.e2e_per_class} instances of each size class per rank, chunks of {CH}"
+        return run, sum(4 * c * n * n * w for n, c in k.items()), sum(c * (n * n + 1) * w for n, c in k.items())
 
 
 class Config5b(Workload):
@@ -660,39 +997,43 @@ class Config5b(Workload):
     workload = ("row-sharded float64 32768x32768 A,B,C U(-1,1): D = 2*A + B % C - A / (1 + abs(B)) on each rank's "
                 "row block (no communication) and trace(A*B) from the rank's A rows / B columns + one NCCL "
                 "all-reduce of one float64")
-    SEEDS = {"A": 51, "B": 52, "C": 53}
     cpu_rows = 256
     cpu_sample_desc = "a 256-row block (config-1 program on 256 x 32768 + its trace partial)"
     e2e_rows = 1024
 
-    def _ws(self):
-        return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+    @staticmethod
+    def seed(name):
+        from paper_2502_03000_b200.datagen import seed_for
+        return seed_for(5, 50 + "ABC".index(name))
 
     def work_per_step(self):
         n = self.N
         return 4 * n * n * 8 + 2 * n * n * 8  # total over all ranks (strong scaling)
 
     def host_inputs(self):
-        rng = np.random.default_rng(1000003 * 42 + 101 * 5 + 50)
+        rng = np.random.default_rng(1000003 * 42 + 101 * 5 + 60)
         r, n = self.cpu_rows, self.N
         return {"A": np.asfortranarray(rng.uniform(-1, 1, (r, n))), "B": np.asfortranarray(rng.uniform(-1, 1, (r, n))),
                 "C": np.asfortranarray(rng.uniform(-1, 1, (r, n))), "Bc": np.asfortranarray(rng.uniform(-1, 1, (n, r)))}
 
     def setup(self, lm, host):
+        import torch
+        from paper_2502_03000_b200.datagen import fill_seeded
         from paper_2502_03000_b200.matrix import fortran_empty
-        from paper_2502_03000_b200.shard import ShardedTrace, fill_uniform, row_range
-        ws, rank = self._ws()
+        from paper_2502_03000_b200.shard import ShardedTrace, row_range
+        ws, rank = _ws()
         n = self.N
         lo, hi = row_range(n, rank, ws)
+        self.lo, self.hi = lo, hi
         blk = {}
-        for k in "ABC":
-            blk[k] = fill_uniform(fortran_empty(hi - lo, n), self.SEEDS[k], lo, 0, n)
-        blk["Bc"] = blk["B"] if ws == 1 else fill_uniform(fortran_empty(n, hi - lo), self.SEEDS["B"], 0, lo, n)
+        for k in "ABC":  # rows [lo, hi) of the row-major draw stream of an n x n matrix
+            blk[k] = fill_seeded(fortran_empty(hi - lo, n), self.seed(k), skip=lo * n, row_stream=n)
+        blk["Bc"] = blk["B"] if ws == 1 else fill_seeded(fortran_empty(n, hi - lo), self.seed("B"), skip=lo,
+                                                         row_stream=n)
         mats = {k: lm.DenseMatrix(blk[k]) for k in "ABC"}
         plan = lm.rewrite(2 * mats["A"] + mats["B"] % mats["C"] - mats["A"] / (1 + abs(mats["B"])))
-        import torch
-        return {"blk": blk, "plan": plan, "trace": ShardedTrace(), "s": torch.empty(1, dtype=torch.float64,
-                                                                                     device="cuda")}
+        return {"blk": blk, "plan": plan, "trace": ShardedTrace(),
+                "s": torch.empty(1, dtype=torch.float64, device="cuda")}
 
     def step_fn(self, lm, ctx):
         def step():
@@ -700,6 +1041,37 @@ class Config5b(Workload):
             s = ctx["trace"](ctx["blk"]["A"], ctx["blk"]["Bc"], ctx["s"])
             return [d, s]
         return step
+
+    def verify(self, lm, ctx, h, outs, O):
+        """Sampled rows of D bitwise vs the oracle program on the same rows
+        regenerated on the host with numpy; a 64-row block's trace partial
+        (device kernel on the resident block) vs the oracle on its host
+        copy."""
+        from paper_2502_03000_b200 import kernels as K
+        from paper_2502_03000_b200.datagen import host_draws
+        from paper_2502_03000_b200.kernels import parse_program
+        import torch
+        ops, args, *_ = parse_program("x0 c0 * x1 x2 * + x0 x1 abs c1 + / -")
+        n, lo, hi = self.N, self.lo, self.hi
+        D = outs[0].data
+        rows = sorted({0, 1, (hi - lo) // 2, hi - lo - 1})
+        rows_ok = True
+        for r in rows:
+            src = [np.asfortranarray(host_draws(self.seed(k), (lo + r) * n, n).reshape(1, n)) for k in "ABC"]
+            ref = np.empty((1, n), order="F")
+            O.program(ops.numpy(), args.numpy(), [2.0, 1.0], src, ref)
+            rows_ok &= _bitwise(D[r:r + 1, :].cpu().numpy(), ref)
+        b = ctx["blk"]
+        r0 = (hi - lo) // 3
+        part = torch.empty(1, dtype=torch.float64, device="cuda")
+        K.trace_of_product(b["A"][r0:r0 + 64, :], b["Bc"][:, r0:r0 + 64], out=part)
+        Ah = b["A"][r0:r0 + 64, :].cpu().numpy()
+        Bh = b["Bc"][:, r0:r0 + 64].cpu().numpy()
+        tr = O.trace_of_product(np.asfortranarray(Ah), np.asfortranarray(Bh))
+        rel = abs(float(part.item()) - tr) / abs(tr)
+        return rows_ok and rel <= 1e-12, {"D_rows_bitwise": len(rows), "rows_ok": bool(rows_ok),
+                                          "trace_block_rel_err": rel, "tol": 1e-12,
+                                          "size": f"full 32768-wide rows, rank block [{lo}, {hi})"}
 
     def kernels_for_roofline(self, lm, ctx):
         from paper_2502_03000_b200 import kernels as K
@@ -751,7 +1123,7 @@ class Config5b(Workload):
 class Config5a32(Config5a):
     config = "5a-f32"
     dtype = "f32"
-    workload = Config5a.workload.replace("U(-1,1)", "U(-1,1), float32")
+    workload = Config5a.workload.replace("U(-1,1) float64", "U(-1,1) float32 (float64 draws rounded)")
 
 
 WORKLOADS = {"1": Config1, "2": Config2, "3a": Config3a, "3b": Config3b, "3c": Config3c, "4a": Config4a,
@@ -785,6 +1157,16 @@ def _max_over_ranks(x: float, ws: int) -> float:
     return float(t.item())
 
 
+def _all_true(ok, ws: int) -> bool:
+    if ws == 1:
+        return bool(ok)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
 def time_cpu(O, wl, host, budget_s: float = 10.0, min_steps: int = 1, max_steps: int = 1000):
     """Run the C restatement of the reference loops for ~budget_s."""
     t0 = time.perf_counter()
@@ -794,6 +1176,22 @@ def time_cpu(O, wl, host, budget_s: float = 10.0, min_steps: int = 1, max_steps:
         steps += 1
     el = time.perf_counter() - t0
     return steps, el
+
+
+def cpu_pool_rate(wl, budget_s: float, workers: int) -> dict:
+    """All-core rate of the oracle over independent instances (process pool)."""
+    pool = CpuPool(wl.config, workers)
+    try:
+        one = pool.step(1)  # warm-up round (page-in, caches)
+        rounds = max(1, int(budget_s / max(one, 1e-3)))
+        el = pool.step(rounds)
+    finally:
+        pool.close()
+    work = wl.pool_work_round() * workers * rounds
+    return {"value": work / el / wl.scale(), "unit": wl.unit, "cores": workers, "kind": "port",
+            "sample": f"{rounds} rounds x {workers} processes ({el:.1f} s); per process per round "
+                      f"{getattr(wl, 'POOL_SAMPLE', None) or getattr(wl, 'POOL_SYSTEMS', '')} instances, "
+                      f"oracle/lm_oracle.c"}
 
 
 def _default_setup(wl, lm, host):
@@ -848,16 +1246,46 @@ def _time_device(fn, steps):
     return e0.elapsed_time(e1) / steps
 
 
+def _cpu_baseline(args, wl, host):
+    from oracle import lm_oracle as O
+    cores = _host_cores()
+    steps, el = time_cpu(O, wl, host, budget_s=args.cpu_budget)
+    cpu = {"value": wl.cpu_work_per_step() * steps / el / wl.scale(), "unit": wl.unit, "cores": 1,
+           "host_cores": cores, "kind": "port",
+           "sample": f"{steps} steps ({el:.1f} s) of {getattr(wl, 'cpu_sample_desc', 'the same workload')}, "
+                     f"oracle/lm_oracle.c (the reference loops restated in C), single thread: 1 of {cores} cores "
+                     f"(the reference is single-threaded, SPEC.md:317)"}
+    if wl.pool and not args.no_pool:
+        cpu["all_cores"] = cpu_pool_rate(wl, args.cpu_budget, cores)
+    return cpu
+
+
 def run_ours(args, wl, ws, rank, local):
+    # the CPU baseline runs first: its process pool forks before this
+    # process creates a CUDA context
+    host = wl.host_inputs()
+    cpu = None
+    if not args.no_cpu and ws == 1 and rank == 0:
+        cpu = _cpu_baseline(args, wl, host)
+
     import torch
 
     import paper_2502_03000_b200 as lm
     from paper_2502_03000_b200 import _native
 
     torch.cuda.set_device(local)
-    host = wl.host_inputs()
     ctx = wl.setup(lm, host) if hasattr(wl, "setup") else _default_setup(wl, lm, host)
     step = wl.step_fn(lm, ctx) if hasattr(wl, "step_fn") else _default_step(wl, lm, ctx)
+
+    # verify before timing: the step's own outputs against the oracle
+    verified, vinfo = None, None
+    if not args.no_verify:
+        from oracle import lm_oracle as O
+        outs = step()
+        torch.cuda.synchronize()
+        ok, vinfo = wl.verify(lm, ctx, host, outs, O)
+        del outs
+        verified = _all_true(ok, ws) if ok is not None else None
 
     sampler = ClockSampler(local, enabled=not args.no_clocks)
     with sampler:
@@ -912,7 +1340,8 @@ def run_ours(args, wl, ws, rank, local):
 
     e2e = None
     if not args.no_e2e:
-        run, h2d, d2h = wl.e2e_fn(lm, host) if hasattr(wl, "e2e_fn") else _default_e2e(wl, lm, host)
+        run, h2d, d2h = (wl.e2e_fn(lm, ctx if wl.config in ("5a", "5a-f32") else host) if hasattr(wl, "e2e_fn")
+                         else _default_e2e(wl, lm, host))
         for _ in range(2):
             run()
         _barrier(ws)
@@ -921,23 +1350,15 @@ def run_ours(args, wl, ws, rank, local):
         for _ in range(k_e2e):
             run()
         el = _max_over_ranks((time.perf_counter() - t0) / k_e2e, ws)
-        work = getattr(wl, "e2e_work", wl.work_per_step())
+        work = getattr(wl, "e2e_work", None)
+        if work is None:
+            work = wl.work_per_step() if wl.scaling == "weak" else wl.work_per_step() / ws
         e2e = {"value": work * ws / el / wl.scale(), "unit": wl.unit, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": el * 1e3, "steps": k_e2e,
-               "includes": "pinned-host inputs H2D, evaluate (rewrite + device scans + kernels), results D2H"}
-        if hasattr(wl, "e2e_work"):
-            e2e["sample"] = (f"{wl.e2e_sample} through the API per step (bounded host memory)"
-                             if isinstance(wl.e2e_sample, str) else
-                             f"{wl.e2e_sample} instances per size class through the API per step")
-
-    cpu = None
-    if not args.no_cpu and ws == 1 and rank == 0:
-        from oracle import lm_oracle as O
-        steps, el = time_cpu(O, wl, host, budget_s=args.cpu_budget)
-        cpu = {"value": wl.cpu_work_per_step() * steps / el / wl.scale(), "unit": wl.unit, "cores": 1,
-               "kind": "port",
-               "sample": f"{steps} steps ({el:.1f} s) of {getattr(wl, 'cpu_sample_desc', 'the same workload')}, "
-                         f"oracle/lm_oracle.c (the reference loops restated in C), single thread"}
+               "includes": "pinned-host inputs H2D, evaluate / batch API (rewrite + device scans + kernels), "
+                           "results D2H"}
+        if hasattr(wl, "e2e_sample"):
+            e2e["sample"] = f"{wl.e2e_sample} through the API per step (bounded pinned host memory)"
 
     roof = None
     if kern:
@@ -954,8 +1375,6 @@ def run_ours(args, wl, ws, rank, local):
             achieved, unit = work / (kms * 1e-3) / 1e9, "GB/s"
             if kflops is not None:
                 fpeak, fkind = _fp64_peak() if wl.dtype == "f64" else _tf32x3_peak()
-                if getattr(wl, "exact_fp64", False):
-                    fpeak, fkind = fpeak / 2, fkind + "; /2 for exact mul+sub (no FMA)"
                 fach = kflops / (kms * 1e-3) / 1e12
                 if fach / fpeak > achieved / peak:  # the kernel is compute-bound: report that roofline
                     work, achieved, peak, peak_kind, unit = kflops, fach, fpeak, fkind, "TFLOP/s"
@@ -973,63 +1392,107 @@ def run_ours(args, wl, ws, rank, local):
             roof["note"] = ("FP64 (DMMA/DFMA) ceiling; sm_100a has no tcgen05 f64 kind" if wl.dtype == "f64" else
                             "f32 products on TF32 tensor cores (3xTF32, FFMA-level accuracy)")
 
-    strong = getattr(wl, "scaling", "weak") == "strong"
+    strong = wl.scaling == "strong"
     total_work = wl.work_per_step() * (1 if strong else ws)
+    parallelism = "single GPU" if ws == 1 else (
+        f"{ws} ranks, " + ("instance partition balanced by realised n^3, no collective" if wl.config in
+                           ("4b", "5a", "5a-f32") else "row shards + one NCCL scalar all-reduce" if strong
+                           else "independent replicas"))
     out = {"metric": METRIC, "value": total_work / (ms_max * 1e-3) / wl.scale(), "unit": wl.unit,
            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
            "dtype": wl.dtype,
-           "data": "synthetic: seeded U(-1,1) (SURVEY.md 8(d)); no public dataset",
+           "data": "synthetic: seeded U(-1,1) (SURVEY.md 8(d)), numpy-identical draws generated on the device; "
+                   "no public dataset",
            "config": {"workload": wl.workload, "baseline_config": wl.config, "work_per_step": wl.work_per_step(),
                       "l2": "working set per step > 126 MB L2; no flush needed",
-                      "parallelism": "replicas" if ws > 1 else "single GPU",
+                      "parallelism": parallelism,
                       "timing": ("CUDA events around CUDA-graph replays of the compiled plans" if wl.graphable
                                  else "CUDA events around evaluate() calls (host syncs inside)")},
-           "impl": "ours", "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+           "impl": "ours", "verified": verified, "verify": vinfo, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
            "clocks": sampler.summary(), "gpu_launches": launches_per_step * args.steps}
     if hasattr(wl, "flops_per_step"):
         out["config"]["flops_per_step"] = wl.flops_per_step()
-        out["tflops"] = wl.flops_per_step() * ws / (ms_max * 1e-3) / 1e12
+        out["tflops"] = wl.flops_per_step() * (1 if strong else ws) / (ms_max * 1e-3) / 1e12
     return out
 
 
 def run_reference(args, wl, ws, rank):
-    """Reference arm: the reference's loops (C restatement, oracle/) on the host cores."""
+    """Reference arm: the reference's loops (C restatement, oracle/) on the
+    host cores -- every core for the batched configs (independent
+    instances, one process each), one core otherwise (the reference
+    algorithm is single-threaded, SPEC.md:317)."""
     if rank != 0:
         return None
-    from oracle import lm_oracle as O
-    host = wl.host_inputs()
-    for _ in range(args.warmup):
-        wl.cpu_step(O, host)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        wl.cpu_step(O, host)
-    el = (time.perf_counter() - t0) / args.steps
-    v = wl.cpu_work_per_step() / el / wl.scale()
+    cores = _host_cores()
+    if wl.pool:
+        pool = CpuPool(wl.config, cores)
+        try:
+            for _ in range(args.warmup):
+                pool.step(1)
+            el = sum(pool.step(1) for _ in range(args.steps)) / args.steps
+        finally:
+            pool.close()
+        v = wl.pool_work_round() * cores / el / wl.scale()
+        used = cores
+        sample = (f"{args.steps} steps; each step one round on {cores} processes, per process "
+                  f"{getattr(wl, 'POOL_SAMPLE', None) or getattr(wl, 'POOL_SYSTEMS', '')} instances; "
+                  f"oracle/lm_oracle.c (the reference's numba loops restated in C)")
+    else:
+        from oracle import lm_oracle as O
+        host = wl.host_inputs()
+        for _ in range(args.warmup):
+            wl.cpu_step(O, host)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            wl.cpu_step(O, host)
+        el = (time.perf_counter() - t0) / args.steps
+        v = wl.cpu_work_per_step() / el / wl.scale()
+        used = 1
+        sample = (f"{args.steps} steps of {getattr(wl, 'cpu_sample_desc', 'the full workload')}, oracle/lm_oracle.c "
+                  f"(the reference's numba loops restated in C), single thread like the reference: 1 of {cores} cores")
     return {"metric": METRIC, "value": v, "unit": wl.unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None,
             "dtype": wl.dtype, "data": "synthetic: seeded U(-1,1) (SURVEY.md 8(d))",
             "config": {"workload": wl.workload, "baseline_config": wl.config, "work_per_step": wl.work_per_step()},
             "impl": "reference",
-            "cpu_baseline": {"value": v, "unit": wl.unit, "cores": 1, "kind": "port",
-                             "sample": f"{args.steps} full steps, oracle/lm_oracle.c (the reference's numba loops "
-                                       f"restated in C, single thread like the reference)"},
+            "cpu_baseline": {"value": v, "unit": wl.unit, "cores": used, "host_cores": cores, "kind": "port",
+                             "sample": sample},
             "e2e": {"value": v, "unit": wl.unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(args, argv) -> int:
+    """`--gpus N` without torchrun: launch N ranks (one per GPU) ourselves."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(pathlib.Path(__file__).resolve()),
+           *argv]
+    return subprocess.call(cmd)
+
+
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pool", action="store_true", help="skip the all-core CPU pool")
+    ap.add_argument("--no-verify", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-clocks", action="store_true", help="skip the NVML clock sampler thread")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args, argv))
     ws, rank, local = _dist()
     wl = WORKLOADS[args.config]()
     if args.impl == "reference":
@@ -1041,13 +1504,15 @@ def main(argv=None):
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     out = run_ours(args, wl, ws, rank, local)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if ws > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    if out.get("verified") is False:
+        sys.exit(3)  # a wrong result is not a benchmark number
 
 
 if __name__ == "__main__":

@@ -67,6 +67,10 @@ const char *lm_last_error(void);
 /* Number of kernels this library has launched since load (for the
  * bench's gpu_launches claim). */
 int64_t lm_launch_count(void);
+/* Name of the kernel variant the calling thread's last multi-variant call
+ * launched (e.g. "stream_tma", "tc05p64"; "" if none): lets tests prove
+ * that an environment switch selected the kernel it names. */
+const char *lm_last_variant(void);
 
 /* ---- element-wise family: _loops.py:37-84 (_fused1.._fused4, _fused_axpy) */
 /* out = sum_k coeffs[k] * srcs[k], accumulated left to right per element,
@@ -173,6 +177,19 @@ int lm_expr_atb_schur_trace_batched(int dtype, int64_t n, int64_t batch, const v
  * distributed matrix can be generated consistently on any rank. */
 int lm_fill_uniform(int dtype, lm_view out, uint64_t seed, int64_t row0, int64_t col0, int64_t global_rows,
                     double lo, double hi, void *stream);
+
+/* numpy-identical seeded fill: element (b, i, j) of `batch` column-major
+ * rows x cols matrices (element at out[b*bstride + i + j*ld]) is draw number
+ * skip + b*bstream + i*rstream + j of np.random.default_rng(seed) (PCG64),
+ * mapped as numpy's uniform(lo, hi) does (lo + (hi - lo) * next_double);
+ * f32 output is that f64 value rounded to nearest.  (state, inc) is the
+ * generator's 128-bit state right after seeding (bit_generator.state).
+ * With bstream = rows*cols and rstream = cols this reproduces
+ * np.asfortranarray(default_rng(seed).uniform(lo, hi, (batch, rows, cols)))
+ * bit for bit -- the SURVEY.md 8(d) operand scheme, generated in HBM. */
+int lm_fill_pcg64(int dtype, void *out, int64_t batch, int64_t rows, int64_t cols, int64_t ld, int64_t bstride,
+                  int64_t bstream, int64_t rstream, uint64_t skip, uint64_t state_hi, uint64_t state_lo,
+                  uint64_t inc_hi, uint64_t inc_lo, double lo, double hi, void *stream);
 
 /* ---- diagnostics ---------------------------------------------------------- */
 /* Factor one LU panel with the cluster kernel, recording clock64() per

@@ -27,13 +27,14 @@ F64, F32 = 0, 1
 
 # Every symbol include/lm_b200.h declares (checked by tests/test_boundary.py).
 EXPORTS = (
-    "lm_abi_version", "lm_last_error", "lm_launch_count",
+    "lm_abi_version", "lm_last_error", "lm_launch_count", "lm_last_variant",
     "lm_fused_axpby", "lm_fused_program", "lm_program_source", "lm_copy", "lm_vec_sum",
     "lm_gemm", "lm_gemv", "lm_syrk",
     "lm_diag_scale", "lm_diag_of_product", "lm_trace_of_product", "lm_triple_diag_dot",
     "lm_analyze", "lm_lu_factor", "lm_lu_solve", "lm_band_solve", "lm_tri_solve",
     "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
     "lm_lu_solve_batched", "lm_solve_batched_classified", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
+    "lm_fill_pcg64",
     "lm_debug_lu_panel",
 )
 
@@ -52,6 +53,7 @@ _SIGS = {
     "lm_abi_version": (_i, []),
     "lm_last_error": (ctypes.c_char_p, []),
     "lm_launch_count": (_i64, []),
+    "lm_last_variant": (ctypes.c_char_p, []),
     "lm_fused_axpby": (_i, [_i, _i, ctypes.POINTER(_d), ctypes.POINTER(View), View, _p]),
     "lm_fused_program": (_i, [_i, _i, _p, _p, _i, ctypes.POINTER(_d), _i, ctypes.POINTER(View), View, _p]),
     "lm_program_source": (_i, [_i, _i, _i, _p, _p, _i, _i, ctypes.c_char_p, _i64]),
@@ -77,6 +79,8 @@ _SIGS = {
     "lm_analyze_batched": (_i, [_i, _i64, _i64, _p, _p, _p]),
     "lm_expr_atb_schur_trace_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "lm_fill_uniform": (_i, [_i, View, ctypes.c_uint64, _i64, _i64, _i64, _d, _d, _p]),
+    "lm_fill_pcg64": (_i, [_i, _p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_uint64,
+                           ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _d, _d, _p]),
     "lm_debug_lu_panel": (_i, [View, _i64, _i, _p, _p, _p, _p]),
 }
 
@@ -108,6 +112,11 @@ def load_library(require_device: bool = True):
 
 def launch_count() -> int:
     return int(load_library(False).lm_launch_count()) if LIB_PATH.exists() else 0
+
+
+def last_variant() -> str:
+    """Kernel variant of this thread's last multi-variant call (lm_last_variant)."""
+    return load_library(False).lm_last_variant().decode()
 
 
 def dtype_code(t: torch.Tensor) -> int:

@@ -158,9 +158,11 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
     return BatchSolveResult(x, cls)
 
 
-def atb_schur_trace(A, B, C, D):
+def atb_schur_trace(A, B, C, D, out=None):
     """E_i = A_i.T @ B_i + C_i % D_i and s_i = trace(A_i @ B_i) for one
-    size class (all instances n x n).  Returns (E, s)."""
+    size class (all instances n x n).  Returns (E, s); ``out=(E, s)``
+    writes into caller-provided buffers (E per-instance F-order like the
+    operands, s a contiguous vector)."""
     for t, nm in ((A, "A"), (B, "B"), (C, "C"), (D, "D")):
         _check_batch(t, f"atb_schur_trace {nm}")
     bt, n, n2 = A.shape
@@ -168,8 +170,17 @@ def atb_schur_trace(A, B, C, D):
         raise KernelContractError("atb_schur_trace: all operands must be (batch, n, n)")
     if len({A.dtype, B.dtype, C.dtype, D.dtype}) != 1:
         raise KernelContractError("atb_schur_trace: operands must share one element type")
-    E = empty_batch(bt, n, n, A.dtype, A.device)
-    s = torch.empty(bt, dtype=A.dtype, device=A.device)
+    if out is None:
+        E = empty_batch(bt, n, n, A.dtype, A.device)
+        s = torch.empty(bt, dtype=A.dtype, device=A.device)
+    else:
+        E, s = out
+        _check_batch(E, "atb_schur_trace E")
+        if tuple(E.shape) != (bt, n, n) or E.dtype != A.dtype:
+            raise KernelContractError("atb_schur_trace: out E must be (batch, n, n) of the operands' type")
+        if s.dim() != 1 or s.shape[0] != bt or s.dtype != A.dtype or (bt > 1 and s.stride(0) != 1):
+            raise KernelContractError("atb_schur_trace: out s must be a contiguous (batch,) vector")
+        N._dev_check(s)
     N.call("lm_expr_atb_schur_trace_batched", N.dtype_code(A), n, bt, A.data_ptr(), B.data_ptr(), C.data_ptr(),
            D.data_ptr(), E.data_ptr(), s.data_ptr())
     return E, s

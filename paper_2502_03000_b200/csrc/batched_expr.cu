@@ -1644,15 +1644,12 @@ int launch_tc05(int64_t batch, const float *a, const float *b, const float *c, c
                 cudaStream_t st) {
     auto kern = atb_schur_trace_tc05;
     const size_t smem = sizeof(SmemTc05) + 1024;  // + alignment slack
-    static int grid = 0;
-    if (!grid) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        grid = 2 * num_sms();  // two CTAs per SM fit; the occupancy API answers 1 (see launch_tc05t)
-    }
+    if (int rc = func_attrs(kern, smem, 100)) return rc;
+    const int grid = 2 * num_sms();  // two CTAs per SM fit; the occupancy API answers 1 (see launch_tc05t)
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 256, smem, st>>>(batch, a, b, c, d, e, s);
     LM_LAUNCHED(1);
+    note_variant("tc05");
     return 0;
 }
 
@@ -1660,14 +1657,18 @@ int launch_stream_f32(int64_t batch, const float *a, const float *b, const float
                       float *s, cudaStream_t st) {
     auto kern = atb_schur_trace_stream_f32;
     const size_t smem = sizeof(SmemStreamF);
-    static int grid = 0;
-    if (!grid) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = resident_grid(kern, 512, smem);
-    }
+    static PerDevice<int> grids;
+    int grid = 0;
+    if (int rc = grids.get(grid, [&](int &g) {
+            if (int rc = func_attrs(kern, smem)) return rc;
+            g = resident_grid(kern, 512, smem);
+            return 0;
+        }))
+        return rc;
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 512, smem, st>>>(batch, a, b, c, d, e, s);
     LM_LAUNCHED(1);
+    note_variant("stream_f32");
     return 0;
 }
 
@@ -1703,14 +1704,18 @@ int launch_stream_tma(int64_t batch, const double *a, const double *b, const dou
     if (batch * HN > 0x7fffffff || !rows_tensor_map(&ta, a, batch) || !rows_tensor_map(&tb, b, batch)) return 1;
     auto kern = atb_schur_trace_stream_tma;
     const size_t smem = sizeof(SmemStreamT) + 512;  // + alignment slack
-    static int grid = 0;
-    if (!grid) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = resident_grid(kern, 512, smem);
-    }
+    static PerDevice<int> grids;
+    int grid = 0;
+    if (int rc = grids.get(grid, [&](int &g) {
+            if (int rc = func_attrs(kern, smem)) return rc;
+            g = resident_grid(kern, 512, smem);
+            return 0;
+        }))
+        return rc;
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 512, smem, st>>>(batch, a, b, c, d, e, s, ta, tb);
     LM_LAUNCHED(1);
+    note_variant("stream_tma");
     return 0;
 }
 
@@ -1752,16 +1757,13 @@ int launch_tc05p(int64_t batch, const float *a, const float *b, const float *c, 
         return 1;
     auto kern = atb_schur_trace_tc05p<PN>;
     const size_t smem = sizeof(SmemTc05T) + 1024;
-    static int grid = 0;
-    if (!grid) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        grid = 2 * num_sms();  // as launch_tc05t
-    }
+    if (int rc = func_attrs(kern, smem, 100)) return rc;
+    const int grid = 2 * num_sms();  // as launch_tc05t
     const int64_t ng = (batch + HN / PN - 1) / (HN / PN);
     const int64_t g = ng < grid ? ng : grid;
     kern<<<(unsigned)g, 256, smem, st>>>(batch, a, c, d, e, s, ta, tb);
     LM_LAUNCHED(1);
+    note_variant(PN == 64 ? "tc05p64" : "tc05p32");
     return 0;
 }
 
@@ -1771,20 +1773,17 @@ int launch_tc05t(int64_t batch, const float *a, const float *b, const float *c, 
     if (batch * HN > 0x7fffffff || !planes_tensor_map(&ta, a, batch) || !planes_tensor_map(&tb, b, batch)) return 1;
     auto kern = atb_schur_trace_tc05t;
     const size_t smem = sizeof(SmemTc05T) + 1024;
-    static int grid = 0;
-    if (!grid) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        // the whole unified L1/shared array as shared memory: without it the
-        // carveout chosen for one CTA leaves the SM at one CTA (ncu: grid 148)
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        // two CTAs per SM fit (ncu: shared-memory limit 2, registers 3) but the
-        // occupancy API answers 1 for this kernel; LM_TC05_CTAS overrides
-        static const int per = getenv("LM_TC05_CTAS") ? atoi(getenv("LM_TC05_CTAS")) : 2;
-        grid = per * num_sms();
-    }
+    // the whole unified L1/shared array as shared memory: without it the
+    // carveout chosen for one CTA leaves the SM at one CTA (ncu: grid 148)
+    if (int rc = func_attrs(kern, smem, 100)) return rc;
+    // two CTAs per SM fit (ncu: shared-memory limit 2, registers 3) but the
+    // occupancy API answers 1 for this kernel; LM_TC05_CTAS overrides
+    static const int per = getenv("LM_TC05_CTAS") ? atoi(getenv("LM_TC05_CTAS")) : 2;
+    const int grid = per * num_sms();
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 256, smem, st>>>(batch, a, c, d, e, s, ta, tb);
     LM_LAUNCHED(1);
+    note_variant("tc05t");
     return 0;
 }
 
@@ -1793,14 +1792,18 @@ int launch_stream(int64_t batch, const double *a, const double *b, const double 
                   double *s, cudaStream_t st) {
     auto kern = atb_schur_trace_stream;
     const size_t smem = sizeof(SmemStream);
-    static int grid = 0;
-    if (!grid) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        grid = resident_grid(kern, 512, smem);
-    }
+    static PerDevice<int> grids;
+    int grid = 0;
+    if (int rc = grids.get(grid, [&](int &g) {
+            if (int rc = func_attrs(kern, smem)) return rc;
+            g = resident_grid(kern, 512, smem);
+            return 0;
+        }))
+        return rc;
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 512, smem, st>>>(batch, a, b, c, d, e, s);
     LM_LAUNCHED(1);
+    note_variant("stream");
     return 0;
 }
 
@@ -1809,16 +1812,18 @@ template <class T, int N>
 int launch_tc(int64_t batch, const T *a, const T *b, const T *c, const T *d, T *e, T *s, cudaStream_t st) {
     auto kern = atb_schur_trace_tc<T, N>;
     const size_t smem = sizeof(Smem<T, N>);
-    static bool attr = false;
-    if (!attr) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    static int grid = 0;
-    if (!grid) grid = resident_grid(kern, 2 * N, smem);
+    static PerDevice<int> grids;
+    int grid = 0;
+    if (int rc = grids.get(grid, [&](int &g) {
+            if (int rc = func_attrs(kern, smem)) return rc;
+            g = resident_grid(kern, 2 * N, smem);
+            return 0;
+        }))
+        return rc;
     const int64_t g = batch < grid ? batch : grid;
     kern<<<(unsigned)g, 2 * N, smem, st>>>(batch, a, b, c, d, e, s);
     LM_LAUNCHED(1);
+    note_variant(sizeof(T) == 8 ? (N == 32 ? "tc_f64_32" : N == 64 ? "tc_f64_64" : "tc_f64_128") : (N == 32 ? "tc_f32_32" : N == 64 ? "tc_f32_64" : "tc_f32_128"));
     return 0;
 }
 
@@ -1826,9 +1831,10 @@ template <class T>
 int launch_half(int64_t batch, const T *a, const T *b, const T *c, const T *d, T *e, T *s, cudaStream_t st) {
     auto kern = atb_schur_trace_half<T>;
     const size_t smem = sizeof(SmemHalf<T>);
-    static int pairs = 0;
-    if (!pairs) {
-        LM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static PerDevice<int> pair_cache;
+    int pairs = 0;
+    if (int rc = pair_cache.get(pairs, [&](int &pairs) {
+        if (int rc = func_attrs(kern, smem)) return rc;
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(2);
         q.blockDim = dim3(256);
@@ -1843,7 +1849,9 @@ int launch_half(int64_t batch, const T *a, const T *b, const T *c, const T *d, T
         int nc = 0;
         if (cudaOccupancyMaxActiveClusters(&nc, kern, &q) != cudaSuccess || nc < 1) nc = num_sms() / 2;
         pairs = nc;
-    }
+        return 0;
+    }))
+        return rc;
     const int64_t np = batch < pairs ? batch : pairs;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(2 * np));
@@ -1859,25 +1867,32 @@ int launch_half(int64_t batch, const T *a, const T *b, const T *c, const T *d, T
     cfg.numAttrs = 1;
     LM_CUDA(cudaLaunchKernelEx(&cfg, kern, batch, a, b, c, d, e, s));
     LM_LAUNCHED(1);
+    note_variant("half");
     return 0;
 }
 
 template <class T>
 int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T *c, const T *d, T *e, T *s,
                       cudaStream_t st) {
-    const bool aligned = ((uintptr_t)a | (uintptr_t)b) % 16 == 0;
+    // The specialised kernels read A / B with 16-byte TMA / cp.async and
+    // C / D / E with 32-byte vectors (launch_tc's epilogue, the n = 128
+    // stream kernels use 16 B): any operand off that alignment (a strided
+    // view with a storage offset) takes the generic kernel instead.
+    const bool aligned = ((uintptr_t)a | (uintptr_t)b) % 16 == 0 && ((uintptr_t)c | (uintptr_t)d | (uintptr_t)e) % 32 == 0;
+    if constexpr (sizeof(T) == 4) {
+        // n = 32 in groups of four per tcgen05 tile: off by default (A/B
+        // baseline against the FFMA kernel, LM_5A_TC05Q=1)
+        static const int q32 = getenv("LM_5A_TC05Q") ? atoi(getenv("LM_5A_TC05Q")) : 0;
+        if (aligned && n == 32 && q32) {
+            const int rc = launch_tc05p<32>(batch, a, b, c, d, e, s, st);
+            if (rc <= 0) return rc;
+        }
+    }
     if (aligned && n == 32) return launch_tc<T, 32>(batch, a, b, c, d, e, s, st);
     if constexpr (sizeof(T) == 4) {
         static const int p64 = getenv("LM_5A_TC05P") ? atoi(getenv("LM_5A_TC05P")) : 1;
         if (aligned && n == 64 && p64) {
             const int rc = launch_tc05p<64>(batch, a, b, c, d, e, s, st);
-            if (rc <= 0) return rc;
-        }
-        // n = 32 in groups of four measured no faster than the FFMA kernel
-        // (0.41 vs 0.40 ms): off by default
-        static const int q32 = getenv("LM_5A_TC05Q") ? atoi(getenv("LM_5A_TC05Q")) : 0;
-        if (aligned && n == 32 && q32) {
-            const int rc = launch_tc05p<32>(batch, a, b, c, d, e, s, st);
             if (rc <= 0) return rc;
         }
     }
@@ -1912,6 +1927,7 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
     if (aligned && n == 128) return launch_tc<T, 128>(batch, a, b, c, d, e, s, st);
     atb_schur_trace_generic<T><<<(unsigned)batch, 256, 0, st>>>(n, a, b, c, d, e, s);
     LM_LAUNCHED(1);
+    note_variant("generic");
     return 0;
 }
 

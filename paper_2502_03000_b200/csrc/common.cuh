@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <mutex>
+
 #include "lm_b200.h"
 
 namespace lm {
@@ -13,9 +15,48 @@ namespace lm {
 
 void set_error(const char *fmt, ...);
 void clear_error();
+bool has_error();
 void count_launch(int n = 1);
+// Records which kernel variant a multi-variant entry point launched last
+// (lm_last_variant(): tests prove the intended specialisation ran).
+void note_variant(const char *name);
 int num_sms();
 void ensure_pool();
+int current_device();  // cudaGetDevice, or -1
+
+constexpr int kMaxDevices = 64;
+
+// Lazily initialised launch state (grid sizes, stream handles) kept per
+// device: init(value) runs once per device, thread-safe (std::call_once);
+// every caller gets the value and init's status.  A process that drives
+// several GPUs therefore sizes and configures each one separately.
+template <class T> class PerDevice {
+  public:
+    template <class F> int get(T &out, F &&init) {
+        const int dev = current_device();
+        if (dev < 0 || dev >= kMaxDevices) {
+            set_error("no current CUDA device (or device index >= %d)", kMaxDevices);
+            return -2;
+        }
+        std::call_once(once_[dev], [&] { rc_[dev] = init(val_[dev]); });
+        if (rc_[dev] && !has_error()) set_error("launch setup failed earlier on device %d", dev);
+        out = val_[dev];
+        return rc_[dev];
+    }
+
+  private:
+    std::once_flag once_[kMaxDevices];
+    T val_[kMaxDevices] = {};
+    int rc_[kMaxDevices] = {};
+};
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize >= bytes [, carveout])
+// once per (kernel, device); thread-safe.  Kernel attributes are
+// per-device state, so a second GPU in the same process needs its own call.
+int ensure_func_attrs(const void *kernel, int smem_bytes, int carveout = -1);
+template <class K> inline int func_attrs(K kernel, size_t smem_bytes, int carveout = -1) {
+    return ensure_func_attrs(reinterpret_cast<const void *>(kernel), (int)smem_bytes, carveout);
+}
 
 #define LM_REQUIRE(cond, ...)                                                                 \
     do {                                                                                      \

@@ -544,11 +544,7 @@ template <bool A_CM, bool B_CN, bool VA, bool VB, int BKT, int ST>
 int launch_dgemm_kernel(const GemmArgs &g, dim3 grid, cudaStream_t s) {
     auto k = dgemm_dmma<A_CM, B_CN, VA, VB, BKT, ST>;
     constexpr int smem = ST * (stage_doubles<A_CM, BKT>() + stage_doubles<B_CN, BKT>()) * 8;
-    static bool attr = false;
-    if (!attr) {
-        LM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr = true;
-    }
+    if (int rc = func_attrs(k, smem)) return rc;
     LM_CUDA(launch_pdl(k, grid, dim3(kGmThreads), smem, s, g));
     LM_LAUNCHED(1);
     return 0;
@@ -565,15 +561,17 @@ int launch_dgemm_layout(const GemmArgs &g, bool va, bool vb, dim3 grid, cudaStre
 // Resident CTAs of the kernel configuration (all layout variants share the
 // register / shared-memory footprint within a few registers).
 template <int BKT, int ST> int64_t dgemm_resident() {
-    static int64_t r = 0;
-    if (!r) {
+    static PerDevice<int64_t> cache;
+    int64_t r = num_sms();
+    cache.get(r, [](int64_t &r) {
         auto k = dgemm_dmma<false, false, true, true, BKT, ST>;
         constexpr int smem = ST * 2 * stage_doubles<false, BKT>() * 8;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        func_attrs(k, smem);
         int per = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kGmThreads, smem) != cudaSuccess || per < 1) per = 1;
         r = (int64_t)per * num_sms();
-    }
+        return 0;
+    });
     return r;
 }
 

@@ -335,8 +335,7 @@ int launch_trsm(const double *T, int64_t ldt, double *X, int64_t ldx, int nbj, i
     constexpr int CPB = 4;
     const size_t smem = sizeof(double) * ((size_t)nbj * (nbj + 1) + CPB);
     if (smem > 48 * 1024)
-        LM_CUDA(cudaFuncSetAttribute(trsm_block<LOWER, SKIP_ZERO, CPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
+        if (int rc = func_attrs(trsm_block<LOWER, SKIP_ZERO, CPB>, smem)) return rc;
     trsm_block<LOWER, SKIP_ZERO, CPB><<<(unsigned)ceil_div(ncols, CPB), nbj * CPB, smem, s>>>(T, ldt, X, ldx, nbj, ncols,
                                                                                            nullptr);
     LM_LAUNCHED(1);
@@ -373,7 +372,7 @@ int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
         P = (int)ceil_div(h, rp);
         size_t smem = sizeof(double) * ((size_t)rp * (nb + 1) + nb);
         LM_REQUIRE(smem <= 200 * 1024, "lu panel: n too large for the panel slice (%lld)", (long long)n);
-        LM_CUDA(cudaFuncSetAttribute(lu_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (int rc = func_attrs(lu_panel, smem)) return rc;
         PanelArgs a{A, lda, n, j0, nb, rp, P, piv, info, pub.as<double>(), pub.as<double>() + 2 * (size_t)maxP * (2 + kLuNb)};
         void *args[] = {&a};
         LM_CUDA(cudaLaunchCooperativeKernel((const void *)lu_panel, dim3(P), dim3(kPanelThreads), args, smem, s));
@@ -492,7 +491,7 @@ int lu_solve_impl(const double *LU, int64_t n, int64_t lda, const int64_t *piv, 
     const size_t psm = sizeof(int32_t) * n;
     LM_REQUIRE(psm <= 200 * 1024, "lu_solve: n too large for the permutation kernel");
     if (psm > 48 * 1024)
-        LM_CUDA(cudaFuncSetAttribute(perm_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm));
+        if (int rc = func_attrs(perm_apply, psm)) return rc;
     const int64_t ngroups = ceil_div(n, 32);
     Scratch groups;
     if (int rc = groups.alloc(sizeof(int32_t) * ngroups * (64 + 64 + 1), s)) return rc;

@@ -225,11 +225,7 @@ int launch_exact_update_c(const double *A, int64_t lda, const double *B, int64_t
                           int64_t M, int64_t N, int K, cudaStream_t s) {
     constexpr int TM = 16 * RM, TN = 16 * RN;
     const size_t smem = sizeof(double) * 2 * (UK * (TM + 2) + TN * (UK + 2));
-    static bool attr = false;
-    if (!attr) {
-        LM_CUDA(cudaFuncSetAttribute(exact_update_c<RM, RN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    if (int rc = func_attrs(exact_update_c<RM, RN>, smem)) return rc;
     dim3 grid((unsigned)ceil_div(M, TM), (unsigned)ceil_div(N, TN));
     exact_update_c<RM, RN><<<grid, 256, smem, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
     LM_LAUNCHED(1);
@@ -241,12 +237,7 @@ int launch_exact_update(const double *A, int64_t lda, const double *B, int64_t l
                         int64_t N, int K, cudaStream_t s) {
     constexpr int TM = 16 * RM, TN = 16 * RN;
     const size_t smem = sizeof(double) * UK * (TM + 1 + TN + 1);
-    static bool attr = false;
-    if (!attr) {
-        LM_CUDA(cudaFuncSetAttribute(exact_update_t<RM, RN, DESC, SKIP_ZERO>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    if (int rc = func_attrs(exact_update_t<RM, RN, DESC, SKIP_ZERO>, smem)) return rc;
     dim3 grid((unsigned)ceil_div(M, TM), (unsigned)ceil_div(N, TN));
     exact_update_t<RM, RN, DESC, SKIP_ZERO><<<grid, 256, smem, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
     LM_LAUNCHED(1);
@@ -414,11 +405,8 @@ static int laswp(double *A, int64_t lda, int64_t n, const int64_t *piv, int64_t 
     if (ncols <= 0 || cnt <= 0) return 0;
     const size_t sm = sizeof(int32_t) * (size_t)(n - k0);
     LM_REQUIRE(sm <= 200 * 1024, "laswp: n too large");
-    static size_t attr = 0;
-    if (sm > 48 * 1024 && sm > attr) {
-        LM_CUDA(cudaFuncSetAttribute(laswp_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        attr = sm;
-    }
+    if (sm > 48 * 1024)
+        if (int rc = func_attrs(laswp_plan, sm)) return rc;
     laswp_plan<<<1, 1024, sm, s>>>(piv, k0, cnt, n, list);
     LM_LAUNCHED(1);
     laswp_apply<<<(unsigned)ncols, 256, 0, s>>>(A, lda, list, a0, a1, b0);
@@ -451,18 +439,14 @@ struct LuStreams {
 };
 
 static int lu_streams(LuStreams &st) {
-    static LuStreams cache[64];
-    int dev = 0;
-    LM_CUDA(cudaGetDevice(&dev));
-    LM_REQUIRE(dev >= 0 && dev < 64, "device index");
-    if (!cache[dev].hi) {
+    static PerDevice<LuStreams> cache;
+    return cache.get(st, [](LuStreams &c) {
         int least = 0, greatest = 0;
         LM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        LM_CUDA(cudaStreamCreateWithPriority(&cache[dev].hi, cudaStreamNonBlocking, greatest));
-        LM_CUDA(cudaStreamCreateWithPriority(&cache[dev].lo, cudaStreamNonBlocking, least));
-    }
-    st = cache[dev];
-    return 0;
+        LM_CUDA(cudaStreamCreateWithPriority(&c.hi, cudaStreamNonBlocking, greatest));
+        LM_CUDA(cudaStreamCreateWithPriority(&c.lo, cudaStreamNonBlocking, least));
+        return 0;
+    });
 }
 
 // Returns 1 (and does nothing) when the cluster panel is not usable for

@@ -540,14 +540,16 @@ __global__ void __launch_bounds__(PT, 1) lu_panel_cluster(ClusterPanelArgs a) {
 }
 
 static int max_cluster() {
-    static int mc = -1;
-    if (mc < 0) {
+    static PerDevice<int> cache;
+    int mc = 8;
+    cache.get(mc, [](int &mc) {
         mc = 8;
         if (cudaFuncSetAttribute(lu_panel_cluster<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                 cudaSuccess &&
             cudaFuncSetAttribute(lu_panel_cluster<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess)
             mc = 16;
-    }
+        return 0;
+    });
     return mc;
 }
 

@@ -311,11 +311,7 @@ static int lu_solve_wavefront2(const double *LU, int64_t n, int64_t lda, double 
                                cudaStream_t s) {
     const int nblk = (int)ceil_div(n, WB), ngrp = (int)ceil_div(m, G2);
     const size_t smem = sizeof(double) * (2 * WB * WLD + 2 * WB * G2LD);
-    static bool attr = false;
-    if (!attr) {
-        LM_CUDA(cudaFuncSetAttribute(lu_solve_wave2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    if (int rc = func_attrs(lu_solve_wave2, smem)) return rc;
     int per_sm = 0;
     LM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_solve_wave2, WT, smem));
     if ((int64_t)per_sm * num_sms() < (int64_t)nblk * ngrp) return 1;
@@ -323,9 +319,15 @@ static int lu_solve_wavefront2(const double *LU, int64_t n, int64_t lda, double 
     const size_t fb = sizeof(int) * 2 * (size_t)nblk * ngrp;
     if (int rc = flags.alloc(fb, s)) return rc;
     LM_CUDA(cudaMemsetAsync(flags.p, 0, fb, s));
-    static unsigned long long *dbg = nullptr;
-    static bool want = getenv("LM_SOLVE_TRACE") != nullptr;
-    if (want && !dbg) LM_CUDA(cudaMalloc(&dbg, sizeof(unsigned long long) * 2 * 4096));
+    static const bool want = getenv("LM_SOLVE_TRACE") != nullptr;
+    static PerDevice<unsigned long long *> dbg_cache;
+    unsigned long long *dbg = nullptr;
+    if (want)
+        if (int rc = dbg_cache.get(dbg, [](unsigned long long *&p) {
+                LM_CUDA(cudaMalloc(&p, sizeof(unsigned long long) * 2 * 4096));
+                return 0;
+            }))
+            return rc;
     Wave2Args args{LU, lda, n, X, ldx, (int)m, nblk, ngrp, flags.as<int>(), want && nblk <= 2048 ? dbg : nullptr};
     void *kargs[] = {&args};
     LM_CUDA(cudaLaunchCooperativeKernel((const void *)lu_solve_wave2, dim3(nblk * ngrp), dim3(WT), kargs, smem, s));
@@ -354,11 +356,7 @@ int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int6
     if (m > WM) return 1;
     const int nblk = (int)ceil_div(n, WB);
     const size_t smem = sizeof(double) * 3 * WB * WLD;
-    static bool attr = false;
-    if (!attr) {
-        LM_CUDA(cudaFuncSetAttribute(lu_solve_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    if (int rc = func_attrs(lu_solve_wave, smem)) return rc;
     int per_sm = 0;
     LM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lu_solve_wave, WT, smem));
     if ((int64_t)per_sm * num_sms() < nblk) return 1;  // all blocks must be co-resident

@@ -347,8 +347,12 @@ template <class T> int trace_impl(const lm_view &av, const lm_view &bv, void *d_
     // the shared-memory kernel's resident wave is faster (6.25 vs 5.9 TB/s at
     // 4096^2), measured with tools/bw_probe.py.
     if (quads && ntiles > 0 && 2.0 * p * q * sizeof(T) >= 512.0 * (1 << 20)) {
-        static int res = 0;
-        if (!res) res = resident_grid(trace_quads<T, 2>, kRedThreads);
+        static PerDevice<int> res_cache;
+        int res = 0;
+        res_cache.get(res, [](int &r) {
+            r = resident_grid(trace_quads<T, 2>, kRedThreads);
+            return 0;
+        });
         int64_t blocks = (int64_t)res * 8;
         if (blocks > ntiles) blocks = ntiles;
         Scratch part;
@@ -360,9 +364,12 @@ template <class T> int trace_impl(const lm_view &av, const lm_view &bv, void *d_
         return 0;
     }
     auto kern = contig ? trace_tiles<T, true> : trace_tiles<T, false>;
-    static int grid_cache[2] = {0, 0};
-    int &g = grid_cache[contig ? 1 : 0];
-    if (!g) g = resident_grid(kern, kRedThreads);
+    static PerDevice<int> grid_cache[2];
+    int g = 0;
+    grid_cache[contig ? 1 : 0].get(g, [&](int &v) {
+        v = resident_grid(kern, kRedThreads);
+        return 0;
+    });
     int64_t blocks = g;
     if (blocks > ntiles) blocks = ntiles;
     if (blocks < 1) blocks = 1;

@@ -26,7 +26,7 @@ import torch
 from . import kernels
 from .matrix import DenseMatrix
 
-__all__ = ["row_range", "ShardedTrace", "eval_rows", "fill_uniform"]
+__all__ = ["row_range", "ShardedTrace", "eval_rows", "fill_uniform", "partition_by_cost", "class_ranges"]
 
 
 def row_range(n: int, rank: int, world: int) -> tuple:
@@ -36,6 +36,43 @@ def row_range(n: int, rank: int, world: int) -> tuple:
     base, extra = divmod(n, world)
     lo = rank * base + min(rank, extra)
     return lo, lo + base + (1 if rank < extra else 0)
+
+
+def partition_by_cost(costs, world: int) -> list:
+    """Contiguous instance ranges [(lo, hi)] per rank, balanced by cost.
+
+    Independent instances (configs 4b, 5a) shard with no collective
+    (SURVEY.md 8(e)): rank g takes the instances whose cumulative cost
+    (realised n^3 per instance) falls in [g/G, (g+1)/G) of the total, so a
+    fixed batch strong-scales and each rank's share of the work differs
+    from 1/G by at most one instance.  Every instance lands on exactly one
+    rank, in order."""
+    import numpy as np
+    c = np.asarray(costs, dtype=np.float64)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if c.size == 0:
+        return [(0, 0)] * world
+    cum = np.cumsum(c)
+    total = cum[-1]
+    # rank boundary g: the first instance whose cost MIDPOINT passes g/G
+    mid = cum - c / 2
+    cuts = [0] + [int(np.searchsorted(mid, total * g / world, side="left")) for g in range(1, world)] + [c.size]
+    return [(cuts[g], cuts[g + 1]) for g in range(world)]
+
+
+def class_ranges(sizes, lo: int, hi: int, classes) -> dict:
+    """For instances [lo, hi) of a mixed-size batch: {n: (first, count)} --
+    the contiguous range of size-class-n indices (the instance's rank among
+    the class-n instances of the WHOLE batch) this slice covers."""
+    import numpy as np
+    sizes = np.asarray(sizes)
+    out = {}
+    for n in classes:
+        is_n = sizes == n
+        first = int(is_n[:lo].sum())
+        out[n] = (first, int(is_n[lo:hi].sum()))
+    return out
 
 
 def _device_partial(a_rows: torch.Tensor, b_cols: torch.Tensor, out: torch.Tensor) -> None:

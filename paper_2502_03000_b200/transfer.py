@@ -45,6 +45,10 @@ def upload(host: torch.Tensor, dtype=None) -> DenseMatrix:
         out.copy_(host if host.dtype == tdt else host.to(tdt), non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(h2d)
+    # `out` belongs to the compute stream's pool: if the matrix is dropped
+    # before any reader waited on the copy, the allocator must not hand the
+    # block out again while the DMA is still writing it
+    out.record_stream(h2d)
     m = DenseMatrix(out)
     m._ready = ev
     return m
@@ -70,6 +74,7 @@ def upload_into(dst: DenseMatrix, host: torch.Tensor, col0: int = 0) -> DenseMat
         dst.data[:, col0:col0 + host.shape[1]].copy_(host, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(h2d)
+    dst.data.record_stream(h2d)  # as in upload(): no reuse while the DMA writes
     dst._ready = ev
     return dst
 

@@ -19,6 +19,7 @@ import json, sys
 import numpy as np, torch
 sys.path.insert(0, sys.argv[1])
 from paper_2502_03000_b200.batch import atb_schur_trace, stack_fortran
+from paper_2502_03000_b200 import _native
 dt = torch.float64 if sys.argv[2] == "f64" else torch.float32
 import os
 rng = np.random.default_rng(11)
@@ -26,8 +27,10 @@ n = int(os.environ.get("LM_5A_N", "128"))
 bt = 400 if n == 128 else 401
 ops = [rng.uniform(-1, 1, (bt, n, n)) for _ in range(4)]
 E, s = atb_schur_trace(*(stack_fortran(o, dtype=dt) for o in ops))
+variant = _native.last_variant()
 idx = [0, 1, 147, 148, 296, 299, 399]
-print(json.dumps({"E": E[idx].double().cpu().numpy().ravel()[::97].tolist(), "s": s[idx].double().cpu().tolist()}))
+print(json.dumps({"E": E[idx].double().cpu().numpy().ravel()[::97].tolist(), "s": s[idx].double().cpu().tolist(),
+                  "variant": variant}))
 """
 
 
@@ -46,17 +49,22 @@ def close(a, b, tol):
     return np.max(np.abs(a - b)) <= tol * max(np.max(np.abs(b)), 1e-30)
 
 
-@pytest.mark.parametrize("variant", [{"LM_5A_TMA": "0"}, {"LM_5A_STREAM": "0"}])
-def test_f64_variants_agree(variant):
+@pytest.mark.parametrize("variant,kernel", [({"LM_5A_TMA": "0"}, "stream"), ({"LM_5A_STREAM": "0"}, "half")])
+def test_f64_variants_agree(variant, kernel):
     ref = run({}, "f64")
+    assert ref["variant"] == "stream_tma"
     got = run(variant, "f64")
+    assert got["variant"] == kernel  # the switch selected the kernel it names
     assert close(got["E"], ref["E"], 1e-12) and close(got["s"], ref["s"], 1e-12)
 
 
-@pytest.mark.parametrize("variant", [{"LM_5A_TC05": "1"}, {"LM_5A_TC05": "0"}, {"LM_5A_TF32": "0"}])
-def test_f32_variants_agree(variant):
+@pytest.mark.parametrize("variant,kernel", [({"LM_5A_TC05": "1"}, "tc05"), ({"LM_5A_TC05": "0"}, "stream_f32"),
+                                            ({"LM_5A_TF32": "0"}, "tc_f32_128")])
+def test_f32_variants_agree(variant, kernel):
     ref = run({}, "f32")
+    assert ref["variant"] == "tc05t"
     got = run(variant, "f32")
+    assert got["variant"] == kernel
     assert close(got["E"], ref["E"], 1e-5) and close(got["s"], ref["s"], 1e-5)
 
 
@@ -67,4 +75,6 @@ def test_f32_grouped_small_sizes_agree(n):
     instances (a partial last group)."""
     ref = run({"LM_5A_TC05P": "0", "LM_5A_N": str(n)}, "f32")
     got = run({"LM_5A_TC05Q": "1", "LM_5A_N": str(n)}, "f32")
+    assert ref["variant"] == f"tc_f32_{n}"
+    assert got["variant"] == f"tc05p{n}"  # the grouped tcgen05 kernel really ran
     assert close(got["E"], ref["E"], 1e-5) and close(got["s"], ref["s"], 1e-5)
