@@ -645,9 +645,16 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
     const int fr = lane >> 2, fc = lane & 3;
-    // TMA SWIZZLE_64B: 16-byte chunk c of row m lands at chunk c ^ ((m >> 1) & 3);
-    // rows wm + 8i + fr share (m >> 1) & 3 = (fr >> 1) & 3
-    const int sw0 = (((fc >> 1) ^ ((fr >> 1) & 3)) << 1) + (fc & 1), sw4 = sw0 ^ 4;
+    // TMA SWIZZLE_64B: 16-byte chunk c of row m lands at chunk c ^ ((m >> 1) & 3).
+    // A 64-bit fragment load is served per half-warp (fragment rows fr 0-3,
+    // then 4-7), so the four rows a half-warp reads must fall in four
+    // different 8-bank groups: group = (row & 1, (row >> 2) & 1).  Fragment
+    // row fr therefore reads tile row pr = {0,1,4,5,2,3,6,7}[fr] (the C
+    // fragment's rows / columns are permuted the same way when P is stored):
+    // conflict-free (2 wavefronts per LDS.64 instead of 4).
+    auto perm = [](int r) { return (r & 1) | ((r & 2) << 1) | ((r & 4) >> 1); };
+    const int pr = perm(fr);
+    const int sw0 = (((fc >> 1) ^ ((pr >> 1) & 3)) << 1) + (fc & 1), sw4 = sw0 ^ 4;
     const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
     const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
     // epilogue pair of this thread in chunk c: elements e, e+1 with e = 2*(c*512 + tid)
@@ -726,19 +733,29 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
 #pragma unroll
             for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
         double tr = 0.0;
-        double2 cn_, dn_;  // C, D of the previous instance's pair for the next chunk
+        // C, D of the previous instance's pair, PF chunks ahead (shift registers)
+        constexpr int PF = 1;  // 2 or 3 chunks ahead measured no faster
+        double2 cq[PF], dq[PF];
         if (prev) {
-            cn_ = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(0)));
-            dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(0)));
+#pragma unroll
+            for (int f = 0; f < PF; ++f) {
+                cq[f] = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(f)));
+                dq[f] = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(f)));
+            }
         }
         for (int c = 0; c < NCH; ++c, ++gch) {
             const int buf = (int)(gch % TST4);
             if (lane == 0 && warp == (int)(gch % 16) && gch + TST4 - 1 < total) produce(gch + TST4 - 1);
             __syncwarp();
-            double2 cv = cn_, dv = dn_;
-            if (prev && c + 1 < NCH) {
-                cn_ = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(c + 1)));
-                dn_ = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(c + 1)));
+            const double2 cv = cq[0], dv = dq[0];
+#pragma unroll
+            for (int f = 0; f + 1 < PF; ++f) {
+                cq[f] = cq[f + 1];
+                dq[f] = dq[f + 1];
+            }
+            if (prev && c + PF < NCH) {
+                cq[PF - 1] = __ldcs(reinterpret_cast<const double2 *>(C + bp * nn + epi_off(c + PF)));
+                dq[PF - 1] = __ldcs(reinterpret_cast<const double2 *>(D + bp * nn + epi_off(c + PF)));
             }
             mbar_wait(&sm.full[buf], (unsigned)((gch / TST4) & 1));
             const double *as = sm.a[buf];
@@ -748,9 +765,9 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
                 double af[4], bf[4];
                 const int o = kk ? sw4 : sw0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * TKC8 + o];
+                for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + pr) * TKC8 + o];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + fr) * TKC8 + o];
+                for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + pr) * TKC8 + o];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -774,7 +791,8 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
-                for (int u = 0; u < 2; ++u) sm.p[(wn + q * 8 + 2 * fc + u) * SLDP + wm + i * 8 + fr] = acc[i][q][u];
+                for (int u = 0; u < 2; ++u)
+                    sm.p[(wn + q * 8 + perm(2 * fc + u)) * SLDP + wm + i * 8 + pr] = acc[i][q][u];
         // trace: fixed-order block sum
         tr = warp_sum(tr);
         if (lane == 0) sm.red[warp] = tr;
@@ -800,6 +818,456 @@ __global__ void __launch_bounds__(512, 1) atb_schur_trace_stream_tma(int64_t bat
             __stcs(reinterpret_cast<double2 *>(E + bl * nn + epi_off(c)), ev);
         }
     }
+}
+
+// Warp-specialised n = 128 f64 kernel (the default; the TMA kernel above is
+// its A/B baseline, LM_5A_WS=0).  Measured on the TMA kernel: with the
+// epilogue's C / D loads and FP64 ops removed the DMMA pipe goes from 72% to
+// 88% busy (6.3 -> 5.2 ms for 40000 instances), while removing the same
+// amount of E stores or trace work changes nothing: every DMUL / DADD /
+// LDG a DMMA warp issues holds that warp's NEXT DMMAs behind it (in-order
+// issue; the FP64 ALU ops queue on the pipe the DMMAs saturate).  So the
+// work is split by role:
+//   16 MMA warps   only DMMA: wait for the chunk, 2 x 16 mma.sync per warp,
+//                  release it; at the end of an instance park the product in
+//                  shared memory (P) for the epilogue warps;
+//    4 epilogue warps  everything else: lane 0 of warp 16 issues the TMA
+//                  ring (two tensor copies + one bulk copy per chunk, as
+//                  above), all 128 threads compute the chunk's trace terms
+//                  (8 k values of one row each) and, during instance j,
+//                  finish 1/16 of E_{j-1} = P + C % D per chunk with C / D
+//                  prefetched a chunk ahead.
+// Two named barriers per instance hand P over (B1: the epilogue warps are
+// done with P_{j-1}; B2: P_j is written).  96 registers per thread (640
+// threads fill the register file) hold the MMA warps' 64 accumulator
+// registers without spills.
+constexpr int WS_MMA_WARPS = 16, WS_EPI_WARPS = 4, WS_THREADS = 32 * (WS_MMA_WARPS + WS_EPI_WARPS);
+struct alignas(128) SmemStreamW {
+    double a[TST4][HN * TKC8];    // A(k, m): [m][k], dense, TMA SWIZZLE_64B
+    double b[TST4][HN * TKC8];    // B(k, n): [n][k]
+    double ac[TST4][TKC8 * HN];   // A(i, k): [k][i]
+    double p[HN * SLDP];          // product of the instance being finished: [n][m]
+    double red[2][WS_MMA_WARPS];  // trace partials (double-buffered by instance parity)
+    unsigned long long full[TST4], empty[TST4];
+};
+
+__device__ __forceinline__ void named_barrier(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+__global__ void __launch_bounds__(WS_THREADS, 1) atb_schur_trace_stream_ws(int64_t batch, const double *__restrict__ A,
+                                                                        const double *__restrict__ C,
+                                                                        const double *__restrict__ D,
+                                                                        double *__restrict__ E, double *__restrict__ S,
+                                                                        const __grid_constant__ CUtensorMap tmA,
+                                                                        const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SmemStreamW &sm = *reinterpret_cast<SmemStreamW *>(smraw + ((512 - (sm_addr(smraw) & 511)) & 511));
+    constexpr int NCH = HN / TKC8;  // 16 chunks per instance
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
+    const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
+    const int64_t total = J * NCH;
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < TST4; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.full[q])), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.empty[q])), "r"(WS_MMA_WARPS));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp < WS_MMA_WARPS) {
+        // ---------------- MMA warps: DMMA, trace terms, the TMA ring ----------------
+        const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+        const int fr = lane >> 2, fc = lane & 3;
+        // half-warp conflict-free fragment rows (see atb_schur_trace_stream_tma)
+        auto perm = [](int r) { return (r & 1) | ((r & 2) << 1) | ((r & 4) >> 1); };
+        const int pr = perm(fr);
+        const int sw0 = (((fc >> 1) ^ ((pr >> 1) & 3)) << 1) + (fc & 1), sw4 = sw0 ^ 4;
+        auto produce = [&](int64_t gp) {
+            const int s = (int)(gp % TST4);
+            const int64_t u = gp / TST4;
+            if (u > 0) mbar_wait(&sm.empty[s], (unsigned)((u - 1) & 1));
+            const int64_t bi = blockIdx.x + (gp / NCH) * G;
+            const int k0 = (int)(gp % NCH) * TKC8;
+            const unsigned fb = sm_addr(&sm.full[s]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(3u * HN * TKC8 * 8u)
+                         : "memory");
+            const int c1 = (int)(bi * HN);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(sm_addr(sm.a[s])),
+                "l"(&tmA), "r"(k0), "r"(c1), "r"(fb)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(sm_addr(sm.b[s])),
+                "l"(&tmB), "r"(k0), "r"(c1), "r"(fb)
+                : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             sm_addr(sm.ac[s])),
+                         "l"(A + bi * nn + (int64_t)k0 * HN), "r"((unsigned)(HN * TKC8 * 8)), "r"(fb)
+                         : "memory");
+        };
+        // chunk g + TST4 - 1 is issued by lane 0 of warp g % 16 (rotating)
+        if (lane == 0 && warp < TST4 - 1 && warp < total) produce(warp);
+        int64_t gch = 0;
+        for (int64_t j = 0; j < J; ++j) {
+            double acc[4][4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+            double tr = 0.0;
+            for (int c = 0; c < NCH; ++c, ++gch) {
+                const int buf = (int)(gch % TST4);
+                if (lane == 0 && warp == (int)(gch % WS_MMA_WARPS) && gch + TST4 - 1 < total) produce(gch + TST4 - 1);
+                __syncwarp();
+                mbar_wait(&sm.full[buf], (unsigned)((gch / TST4) & 1));
+                const double *as = sm.a[buf];
+                const double *bs = sm.b[buf];
+#pragma unroll
+                for (int kk = 0; kk < TKC8; kk += 4) {
+                    double af[4], bf[4];
+                    const int o = kk ? sw4 : sw0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + pr) * TKC8 + o];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + pr) * TKC8 + o];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) dmma884(acc[i][q], af[i], bf[q]);
+                }
+                {
+                    // trace terms: sum_{k in chunk} sum_i A(i,k) B(k,i); 2 per thread
+                    const double *ac = sm.ac[buf];
+                    const int i = tid & 127, k2 = (tid >> 7) * 2;
+                    const int bo = i * TKC8 + (((k2 >> 1) ^ ((i >> 1) & 3)) << 1);  // k2 even
+                    tr = fma(ac[k2 * HN + i], bs[bo], tr);
+                    tr = fma(ac[(k2 + 1) * HN + i], bs[bo + 1], tr);
+                }
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.empty[buf])) : "memory");
+            }
+            tr = warp_sum(tr);
+            if (lane == 0) sm.red[j & 1][warp] = tr;
+            named_barrier(1, WS_THREADS);  // B1: the epilogue warps are done with P_{j-1}
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u)
+                        sm.p[(wn + q * 8 + perm(2 * fc + u)) * SLDP + wm + i * 8 + pr] = acc[i][q][u];
+            named_barrier(2, WS_THREADS);  // B2: P_j and the trace partials complete
+        }
+        return;
+    }
+
+    // ---------------- epilogue warps: E_{j-1} = P + C % D during instance j ----------------
+    const int et = tid - 32 * WS_MMA_WARPS;
+    // slice c of an instance: elements c*1024 + 2*et + 256*r, r < 4
+    // (column-major; a warp covers 512 contiguous bytes per r)
+    auto load_cd = [&](int64_t bl, int c, double2 (&cv)[4], double2 (&dv)[4]) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int e = c * 1024 + 2 * et + 256 * r;
+            cv[r] = __ldcs(reinterpret_cast<const double2 *>(C + bl * nn + e));
+            dv[r] = __ldcs(reinterpret_cast<const double2 *>(D + bl * nn + e));
+        }
+    };
+    auto slice = [&](int64_t bl, int c, const double2 (&cv)[4], const double2 (&dv)[4]) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int e = c * 1024 + 2 * et + 256 * r, n = e >> 7, m = e & 127;
+            const double2 pv = *reinterpret_cast<const double2 *>(&sm.p[n * SLDP + m]);
+            double2 ev;
+            ev.x = radd(pv.x, rmul(cv[r].x, dv[r].x));
+            ev.y = radd(pv.y, rmul(cv[r].y, dv[r].y));
+            __stcs(reinterpret_cast<double2 *>(E + bl * nn + e), ev);
+        }
+    };
+    // all 16 slices of instance bl, loads two slices ahead
+    auto finish = [&](int64_t bl) {
+        double2 c0[4], d0[4], c1[4], d1[4];
+        load_cd(bl, 0, c0, d0);
+        load_cd(bl, 1, c1, d1);
+#pragma unroll 1
+        for (int c = 0; c < NCH; c += 2) {
+            slice(bl, c, c0, d0);
+            if (c + 2 < NCH) load_cd(bl, c + 2, c0, d0);
+            slice(bl, c + 1, c1, d1);
+            if (c + 3 < NCH) load_cd(bl, c + 3, c1, d1);
+        }
+    };
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t b = blockIdx.x + j * G;
+        if (j > 0) finish(b - G);
+        named_barrier(1, WS_THREADS);  // B1
+        named_barrier(2, WS_THREADS);  // B2
+        if (et == 0) {
+            double t = sm.red[j & 1][0];
+#pragma unroll
+            for (int w = 1; w < WS_MMA_WARPS; ++w) t = radd(t, sm.red[j & 1][w]);
+            S[b] = t;
+        }
+    }
+    if (J > 0) finish(blockIdx.x + (J - 1) * G);  // drain: the last instance
+}
+
+// n = 128 f64 with the finished product parked in TENSOR MEMORY (the
+// default).  The stream kernels above keep the previous instance's product
+// P in a 133 KB shared-memory buffer, which leaves room for a ring of only
+// four 8-row chunks (3 in flight, ~3.5 us of look-ahead): with the C / D /
+// E traffic of the overlapped epilogue the loaded HBM latency exceeds that
+// and the DMMA pipe idles (72% busy; 88% with the epilogue's traffic
+// removed, measured).  DMMA does not use TMEM, so P goes there instead
+// (tcgen05.st / tcgen05.ld, 128 lanes x 256 columns = 128 KB) and the whole
+// shared memory becomes a TM_ST-deep ring.  Roles:
+//   16 MMA warps      DMMA (32 x 32 warp tiles), trace terms, the TMA ring
+//                     (rotating producer lane); at the end of instance j each
+//                     thread stores its 32 accumulators to its own TMEM lane
+//                     (32x32b: lane = 32*(warp%4) + laneid, 64 columns per
+//                     warp column group);
+//    4 epilogue warps  during instance j+1 each reads the TMEM lanes of its
+//                     quarter (a warp may only touch lanes 32*(warp%4)..+31),
+//                     i.e. exactly the fragments of MMA warps e, e+4, e+8,
+//                     e+12, and writes E = P + C % D at those positions, C / D
+//                     loaded one 8-element block ahead.
+// Two named barriers per instance hand P over, as in the kernel above.
+constexpr int TM_ST = 6, TM_CD = 4;
+struct alignas(128) SmemStreamM {
+    double a[TM_ST][HN * TKC8];   // A(k, m): [m][k], dense, TMA SWIZZLE_64B
+    double b[TM_ST][HN * TKC8];   // B(k, n): [n][k]
+    double ac[TM_ST][TKC8 * HN];  // A(i, k): [k][i]
+    double cs[TM_CD][8 * HN];     // epilogue pieces: 8 columns of C ...
+    double ds[TM_CD][8 * HN];     // ... and of D (one 8 KB bulk copy each)
+    double red[2][WS_MMA_WARPS];  // trace partials (double-buffered by instance parity)
+    unsigned long long full[TM_ST], empty[TM_ST], cd_full[TM_CD];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(WS_THREADS, 1) atb_schur_trace_stream_tm(int64_t batch, const double *__restrict__ A,
+                                                                        const double *__restrict__ C,
+                                                                        const double *__restrict__ D,
+                                                                        double *__restrict__ E, double *__restrict__ S,
+                                                                        const __grid_constant__ CUtensorMap tmA,
+                                                                        const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SmemStreamM &sm = *reinterpret_cast<SmemStreamM *>(smraw + ((512 - (sm_addr(smraw) & 511)) & 511));
+    constexpr int NCH = HN / TKC8;  // 16 chunks per instance
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t nn = (int64_t)HN * HN, G = gridDim.x;
+    const int64_t J = batch > (int64_t)blockIdx.x ? (batch - blockIdx.x + G - 1) / G : 0;
+    const int64_t total = J * NCH;
+    if (warp == WS_MMA_WARPS) {  // the first epilogue warp owns the TMEM allocation
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sm_addr(&sm.tmem_base)),
+                     "r"(2 * HN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < TM_ST; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.full[q])), "r"(1));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.empty[q])), "r"(WS_MMA_WARPS));
+        }
+#pragma unroll
+        for (int q = 0; q < TM_CD; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.cd_full[q])), "r"(1));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = sm.tmem_base;
+    auto perm = [](int r) { return (r & 1) | ((r & 2) << 1) | ((r & 4) >> 1); };
+
+    if (warp < WS_MMA_WARPS) {
+        // ---------------- MMA warps: DMMA, trace terms, the TMA ring ----------------
+        // registers: the CTA launched with 96 per thread; the epilogue warps
+        // hand 32 each back, the MMA warps take 8 more (4 x 128 x 8 = 128 x 32)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
+        const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+        const int fr = lane >> 2, fc = lane & 3;
+        const int pr = perm(fr);  // half-warp conflict-free fragment rows (see atb_schur_trace_stream_tma)
+        const int sw0 = (((fc >> 1) ^ ((pr >> 1) & 3)) << 1) + (fc & 1), sw4 = sw0 ^ 4;
+        const uint32_t my_tmem = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+        auto produce = [&](int64_t gp) {
+            const int s = (int)(gp % TM_ST);
+            const int64_t u = gp / TM_ST;
+            if (u > 0) mbar_wait(&sm.empty[s], (unsigned)((u - 1) & 1));
+            const int64_t bi = blockIdx.x + (gp / NCH) * G;
+            const int k0 = (int)(gp % NCH) * TKC8;
+            const unsigned fb = sm_addr(&sm.full[s]);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(3u * HN * TKC8 * 8u)
+                         : "memory");
+            const int c1 = (int)(bi * HN);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(sm_addr(sm.a[s])),
+                "l"(&tmA), "r"(k0), "r"(c1), "r"(fb)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(sm_addr(sm.b[s])),
+                "l"(&tmB), "r"(k0), "r"(c1), "r"(fb)
+                : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             sm_addr(sm.ac[s])),
+                         "l"(A + bi * nn + (int64_t)k0 * HN), "r"((unsigned)(HN * TKC8 * 8)), "r"(fb)
+                         : "memory");
+        };
+        // chunk g + TM_ST - 1 is issued by lane 0 of warp g % 16 (rotating)
+        if (lane == 0 && warp < TM_ST - 1 && warp < total) produce(warp);
+        int64_t gch = 0;
+        for (int64_t j = 0; j < J; ++j) {
+            double acc[4][4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
+            double tr = 0.0;
+            for (int c = 0; c < NCH; ++c, ++gch) {
+                const int buf = (int)(gch % TM_ST);
+                if (lane == 0 && warp == (int)(gch % WS_MMA_WARPS) && gch + TM_ST - 1 < total) produce(gch + TM_ST - 1);
+                __syncwarp();
+                mbar_wait(&sm.full[buf], (unsigned)((gch / TM_ST) & 1));
+                const double *as = sm.a[buf];
+                const double *bs = sm.b[buf];
+#pragma unroll
+                for (int kk = 0; kk < TKC8; kk += 4) {
+                    double af[4], bf[4];
+                    const int o = kk ? sw4 : sw0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + pr) * TKC8 + o];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + pr) * TKC8 + o];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) dmma884(acc[i][q], af[i], bf[q]);
+                }
+                {
+                    // trace terms: sum_{k in chunk} sum_i A(i,k) B(k,i); 2 per thread
+                    const double *ac = sm.ac[buf];
+                    const int i = tid & 127, k2 = (tid >> 7) * 2;
+                    const int bo = i * TKC8 + (((k2 >> 1) ^ ((i >> 1) & 3)) << 1);  // k2 even
+                    tr = fma(ac[k2 * HN + i], bs[bo], tr);
+                    tr = fma(ac[(k2 + 1) * HN + i], bs[bo + 1], tr);
+                }
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(&sm.empty[buf])) : "memory");
+            }
+            tr = warp_sum(tr);
+            if (lane == 0) sm.red[j & 1][warp] = tr;
+            named_barrier(1, WS_THREADS);  // B1: the epilogue warps are done with P_{j-1}
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            // TMEM columns 16 q + 4 i + 2 u (+1 for the high word): the 8
+            // accumulators of one 8-column block q are contiguous
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                uint32_t w[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        w[(i * 2 + u) * 2] = (uint32_t)__double2loint(acc[i][q][u]);
+                        w[(i * 2 + u) * 2 + 1] = (uint32_t)__double2hiint(acc[i][q][u]);
+                    }
+                asm volatile(
+                    "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                    "%16};" ::"r"(my_tmem + (uint32_t)(16 * q)),
+                    "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]),
+                    "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+                    : "memory");
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            named_barrier(2, WS_THREADS);  // B2: P_j and the trace partials complete
+        }
+        return;
+    }
+
+    // ---------------- epilogue warps: E_{j-1} = P + C % D during instance j ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;\n" ::: "memory");
+    const int e4 = warp - WS_MMA_WARPS;  // == warp % 4: TMEM lanes 32*e4 .. +31
+    const int et = tid - 32 * WS_MMA_WARPS;
+    const int fr = lane >> 2, fc = lane & 3;
+    const int m = 32 * e4 + perm(fr);  // + 8 i
+    // Piece p (0..15) of an instance: columns 8p .. 8p+7 of C and D (8 KB
+    // contiguous each: one bulk copy) into slot pc % TM_CD, pc = instance*16 + p
+    // counted over the CTA's whole run; these are the columns 32 g + 8 q of
+    // MMA column group g = p / 4, block q = p % 4 -- one x16 TMEM load.
+    const int64_t total_pieces = J * 16;
+    auto issue = [&](int64_t pc) {
+        const int slot = (int)(pc % TM_CD);
+        const int64_t bl = blockIdx.x + (pc >> 4) * G;
+        const int64_t off = bl * nn + (int64_t)(pc & 15) * 8 * HN;
+        const unsigned fb = sm_addr(&sm.cd_full[slot]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(2u * 8u * HN * 8u)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         sm_addr(sm.cs[slot])),
+                     "l"(C + off), "r"((unsigned)(8 * HN * 8)), "r"(fb)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         sm_addr(sm.ds[slot])),
+                     "l"(D + off), "r"((unsigned)(8 * HN * 8)), "r"(fb)
+                     : "memory");
+    };
+    if (et == 0)
+        for (int64_t pc = 0; pc < TM_CD - 1 && pc < total_pieces; ++pc) issue(pc);
+    int64_t pc = 0;
+    // all 16 pieces of instance bl (P_bl in TMEM)
+    auto finish = [&](int64_t bl) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll 1
+        for (int p = 0; p < 16; ++p, ++pc) {
+            if (et == 0 && pc + TM_CD - 1 < total_pieces) issue(pc + TM_CD - 1);
+            const int slot = (int)(pc % TM_CD);
+            uint32_t w[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]),
+                  "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+                : "r"(tmem + ((uint32_t)(32 * e4) << 16) + (uint32_t)(64 * (p >> 2) + 16 * (p & 3))));
+            mbar_wait(&sm.cd_full[slot], (unsigned)((pc / TM_CD) & 1));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const double *cs = sm.cs[slot], *ds = sm.ds[slot];
+            double *pe = E + bl * nn + (int64_t)p * 8 * HN;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int f = i * 2 + u;
+                    const int o = perm(2 * fc + u) * HN + m + 8 * i;
+                    const double pv = __hiloint2double((int)w[2 * f + 1], (int)w[2 * f]);
+                    __stcs(pe + o, radd(pv, rmul(cs[o], ds[o])));
+                }
+            named_barrier(3, 32 * WS_EPI_WARPS);  // the slot is free for piece pc + TM_CD
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+    };
+    for (int64_t j = 0; j < J; ++j) {
+        const int64_t b = blockIdx.x + j * G;
+        if (j > 0) finish(b - G);
+        named_barrier(1, WS_THREADS);  // B1
+        named_barrier(2, WS_THREADS);  // B2
+        if (tid == 32 * WS_MMA_WARPS) {
+            double t = sm.red[j & 1][0];
+#pragma unroll
+            for (int w = 1; w < WS_MMA_WARPS; ++w) t = radd(t, sm.red[j & 1][w]);
+            S[b] = t;
+        }
+    }
+    if (J > 0) finish(blockIdx.x + (J - 1) * G);  // drain: the last instance
+    named_barrier(4, 32 * WS_EPI_WARPS);  // all four epilogue warps' TMEM reads done before the free
+    if (warp == WS_MMA_WARPS) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * HN));
 }
 
 // n = 128 f32: the same streaming structure with A.T @ B on the TENSOR
@@ -1719,6 +2187,36 @@ int launch_stream_tma(int64_t batch, const double *a, const double *b, const dou
     return 0;
 }
 
+int launch_stream_ws(int64_t batch, const double *a, const double *b, const double *c, const double *d, double *e,
+                     double *s, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    if (batch * HN > 0x7fffffff || !rows_tensor_map(&ta, a, batch) || !rows_tensor_map(&tb, b, batch)) return 1;
+    auto kern = atb_schur_trace_stream_ws;
+    const size_t smem = sizeof(SmemStreamW) + 512;  // + alignment slack
+    if (int rc = func_attrs(kern, smem)) return rc;
+    const int grid = num_sms();  // one 20-warp CTA per SM
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, WS_THREADS, smem, st>>>(batch, a, c, d, e, s, ta, tb);
+    LM_LAUNCHED(1);
+    note_variant("stream_ws");
+    return 0;
+}
+
+int launch_stream_tm(int64_t batch, const double *a, const double *b, const double *c, const double *d, double *e,
+                     double *s, cudaStream_t st) {
+    CUtensorMap ta, tb;
+    if (batch * HN > 0x7fffffff || !rows_tensor_map(&ta, a, batch) || !rows_tensor_map(&tb, b, batch)) return 1;
+    auto kern = atb_schur_trace_stream_tm;
+    const size_t smem = sizeof(SmemStreamM) + 512;  // + alignment slack
+    if (int rc = func_attrs(kern, smem)) return rc;
+    const int grid = num_sms();  // one 20-warp CTA per SM (it owns 256 TMEM columns)
+    const int64_t g = batch < grid ? batch : grid;
+    kern<<<(unsigned)g, WS_THREADS, smem, st>>>(batch, a, c, d, e, s, ta, tb);
+    LM_LAUNCHED(1);
+    note_variant("stream_tm");
+    return 0;
+}
+
 // batch x 128 x 128 column-major f32 instances as a 2D tensor: dim 0 = row k
 // (contiguous, 128), dim 1 = column over all instances; box 4 rows x 128
 // columns (one 16-byte K piece of every column)
@@ -1905,6 +2403,16 @@ int batched_expr_impl(int64_t n, int64_t batch, const T *a, const T *b, const T 
     }();
     if constexpr (sizeof(T) == 8) {
         static const int tma = getenv("LM_5A_TMA") ? atoi(getenv("LM_5A_TMA")) : 1;
+        static const int ws = getenv("LM_5A_WS") ? atoi(getenv("LM_5A_WS")) : 1;
+        static const int tm = getenv("LM_5A_TM") ? atoi(getenv("LM_5A_TM")) : 0;
+        if (aligned && n == 128 && stream128 && tma && ws && tm) {
+            const int rc = launch_stream_tm(batch, a, b, c, d, e, s, st);
+            if (rc <= 0) return rc;
+        }
+        if (aligned && n == 128 && stream128 && tma && ws) {
+            const int rc = launch_stream_ws(batch, a, b, c, d, e, s, st);
+            if (rc <= 0) return rc;  // 1: no tensor-map encoder
+        }
         if (aligned && n == 128 && stream128 && tma) {
             const int rc = launch_stream_tma(batch, a, b, c, d, e, s, st);
             if (rc <= 0) return rc;  // 1: no tensor-map encoder -> the cp.async ring

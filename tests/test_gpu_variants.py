@@ -49,10 +49,11 @@ def close(a, b, tol):
     return np.max(np.abs(a - b)) <= tol * max(np.max(np.abs(b)), 1e-30)
 
 
-@pytest.mark.parametrize("variant,kernel", [({"LM_5A_TMA": "0"}, "stream"), ({"LM_5A_STREAM": "0"}, "half")])
+@pytest.mark.parametrize("variant,kernel", [({"LM_5A_TM": "1"}, "stream_tm"), ({"LM_5A_WS": "0"}, "stream_tma"),
+                                            ({"LM_5A_TMA": "0"}, "stream"), ({"LM_5A_STREAM": "0"}, "half")])
 def test_f64_variants_agree(variant, kernel):
     ref = run({}, "f64")
-    assert ref["variant"] == "stream_tma"
+    assert ref["variant"] == "stream_ws"
     got = run(variant, "f64")
     assert got["variant"] == kernel  # the switch selected the kernel it names
     assert close(got["E"], ref["E"], 1e-12) and close(got["s"], ref["s"], 1e-12)
