@@ -571,7 +571,7 @@ class Config4a(Workload):
     graphable = False
     N, NRHS = 8192, 64
     workload = ("inverse(A)*b -> LU solve (R9), float64 A = U(-1,1) + 8192*I (data leaf), b 8192x64; "
-                "exact reference operation order")
+                "blocked LU with reference pivots, trailing updates on the FP64 tensor cores (DMMA)")
 
     def host_inputs(self):
         n = self.N
@@ -586,7 +586,6 @@ class Config4a(Workload):
         n, k = self.N, self.NRHS
         return 2 * n * n * n // 3 + 2 * n * n * k  # lazymat/kernels.py:190, :215
 
-    exact_fp64 = True
     roofline_graphable = False
 
     def kernels_for_roofline(self, lm, m):
@@ -606,7 +605,7 @@ class Config4a(Workload):
         def solve():
             x.copy_(b)
             N.call("lm_lu_solve", 0, N.view(work), piv.data_ptr(), N.view(x))
-        return [("lu_factor (cluster panels + exact updates)", 2 * n ** 3 // 3, factor),
+        return [("lu_factor (cluster panels + DMMA trailing updates)", 2 * n ** 3 // 3, factor),
                 ("lu_solve (wavefront substitution)", 2 * n * n * k, solve)]
 
     cpu_n = 1024

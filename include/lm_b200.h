@@ -128,6 +128,15 @@ int lm_analyze(int dtype, lm_view a, int square, int64_t *d_out, void *stream);
  * (cs == rows, rs == 1).  d_piv[k] = pivot row of column k (0-based,
  * sequential swap semantics), *d_info = 0 or failing column + 1. */
 int lm_lu_factor(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_info, void *stream);
+/* Trailing-update arithmetic of the blocked LU: LM_LU_EXACT applies every
+ * update in the reference's order with separately rounded multiply and
+ * subtract (values and pivots bit-identical to _lu_factor); LM_LU_TENSOR runs
+ * the trailing updates on the FP64 tensor cores (DMMA, FMA accumulation:
+ * scaled residual <= 1e-10, pivots equal unless two candidates tie to
+ * rounding); LM_LU_AUTO (what lm_lu_factor uses) is exact below n = 2048 and
+ * tensor from there on, overridable with LM_LU_MODE=exact|tensor. */
+enum { LM_LU_AUTO = 0, LM_LU_EXACT = 1, LM_LU_TENSOR = 2 };
+int lm_lu_factor_mode(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_info, int mode, void *stream);
 /* Solve with a factorisation from lm_lu_factor; x (n x m, F-order)
  * arrives holding B and is overwritten with X. */
 int lm_lu_solve(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, void *stream);

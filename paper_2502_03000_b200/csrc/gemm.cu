@@ -297,6 +297,7 @@ struct GemmArgs {
     double *part;    // split-K partials [z][M*N] (F-order), or null
     int syrk;        // 1: only upper tiles (tile index -> (tm <= tn)), mirrored store
     int64_t tiles_n;
+    int sub;         // 1: C -= A B (one rounding per element; never split along K)
 };
 
 // One operand's tile stream (A as (outer = m, k), B as (outer = n, k)).
@@ -489,6 +490,9 @@ __global__ void __launch_bounds__(kGmThreads) dgemm_dmma(GemmArgs g) {
                     if (tm == tn && m > n) continue;
                     g.c[m * g.c_sm + n * g.c_sn] = v;
                     g.c[n * g.c_sm + m * g.c_sn] = v;
+                } else if (g.sub) {
+                    double *pc = g.c + m * g.c_sm + n * g.c_sn;
+                    *pc = __dsub_rn(*pc, v);
                 } else {
                     g.c[m * g.c_sm + n * g.c_sn] = v;
                 }
@@ -608,7 +612,7 @@ int dgemm_cfg(GemmArgs &g, bool a_cm, bool b_cn, bool va, bool vb, cudaStream_t 
     const int64_t tM = ceil_div(M, BM), tN = ceil_div(N, BN);
     const int64_t tiles = g.syrk ? tM * (tM + 1) / 2 : tM * tN;
     g.tiles_n = tN;
-    int64_t splits = choose_splits(tiles, M, N, K, BKT, dgemm_resident<BKT, ST>());
+    int64_t splits = g.sub ? 1 : choose_splits(tiles, M, N, K, BKT, dgemm_resident<BKT, ST>());
     g.kchunk = ceil_div(ceil_div(K, splits), BKT) * BKT;
     splits = ceil_div(K, g.kchunk);
     Scratch part;
@@ -673,6 +677,32 @@ int dgemm(const double *a, int64_t a_sm, int64_t a_sk, const double *b, int64_t 
     // BK 16, 3 stages: 32.3 TF/s on the config-3c SYRK (BK 32 x 2 stages ties,
     // 3-4 deep BK-32/16 rings lose occupancy)
     return dgemm_cfg<16, 3>(g, a_cm, b_cn, va, vb, s);
+}
+
+// C -= A B for column-major A (M x K, lda), B (K x N, ldb), C (M x N, ldc):
+// the blocked LU's trailing update on the FP64 tensor cores (DMMA with FMA
+// accumulation; lu_fast.cu's tensor mode).
+int dgemm_sub(const double *a, int64_t lda, const double *b, int64_t ldb, double *c, int64_t ldc, int64_t M,
+              int64_t N, int64_t K, cudaStream_t s) {
+    if (M <= 0 || N <= 0 || K <= 0) return 0;
+    GemmArgs g{};
+    g.a = a;
+    g.a_sm = 1;
+    g.a_sk = lda;
+    g.b = b;
+    g.b_sk = 1;
+    g.b_sn = ldb;
+    g.c = c;
+    g.c_sm = 1;
+    g.c_sn = ldc;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.sub = 1;
+    auto aligned16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
+    const bool va = aligned16(a) && lda % 2 == 0;
+    const bool vb = aligned16(b) && ldb % 2 == 0;
+    return dgemm_cfg<16, 3>(g, true, false, va, vb, s);
 }
 
 // FP32 (batched-config extension) generic SIMT GEMM, FMA accumulate.

@@ -26,6 +26,7 @@
 // second round trip).  Row swaps of the columns outside the panel are
 // done in the same step by all CTAs (the LAPACK laswp, fused).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -344,7 +345,7 @@ int launch_trsm(const double *T, int64_t ldt, double *X, int64_t ldx, int nbj, i
 
 constexpr int kLuNb = 64;
 
-int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s);
+int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, bool tensor);
 int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s);
 template <bool DESC, bool SKIP_ZERO>
 int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
@@ -352,12 +353,32 @@ int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, dou
 template <bool LOWER>
 int tri32(const double *T, int64_t ldt, double *X, int64_t ldx, int nb, int64_t ncols, cudaStream_t s);
 
-int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
+// Trailing-update arithmetic of the blocked LU (lm_lu_factor_mode):
+// exact reference order below LU_TENSOR_MIN_N (values and pivots bitwise equal
+// to _lu_factor, what the reference-generated goldens pin), the FP64 tensor
+// cores (DMMA, FMA accumulation) from there on, where the north star asks a
+// scaled residual <= 1e-10 and the same pivot indices.  LM_LU_MODE=exact /
+// tensor overrides the automatic choice.
+constexpr int64_t LU_TENSOR_MIN_N = 2048;
+static bool lu_tensor_mode(int mode, int64_t n) {
+    if (mode == LM_LU_EXACT) return false;
+    if (mode == LM_LU_TENSOR) return true;
+    static const int env = [] {
+        const char *e = getenv("LM_LU_MODE");
+        if (!e) return 0;
+        return e[0] == 'e' ? 1 : e[0] == 't' ? 2 : 0;
+    }();
+    if (env) return env == 2;
+    return n >= LU_TENSOR_MIN_N;
+}
+
+int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, int mode) {
     LM_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     if (n == 0) return 0;
     // two-level blocked LU with a thread-block-cluster panel (lu_fast.cu);
     // returns 1 when the panel does not fit a cluster -> cooperative path
-    if (int rc = lu_factor_fast(A, n, lda, piv, info, s); rc != 1) return rc;
+    // (exact order only)
+    if (int rc = lu_factor_fast(A, n, lda, piv, info, s, lu_tensor_mode(mode, n)); rc != 1) return rc;
     const int nsm = num_sms();
     Scratch pub;
     const int maxP = nsm;
@@ -674,7 +695,17 @@ extern "C" int lm_lu_factor(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_in
     LM_REQUIRE(dtype == LM_F64, "lu_factor: f64 only");
     LM_REQUIRE(lu.rows == lu.cols, "lu_factor needs a square matrix");
     LM_REQUIRE(lu.rs == 1 && (lu.cs >= lu.rows || lu.rows <= 1), "lu_factor needs F-order storage");
-    return lu_factor_impl((double *)lu.ptr, lu.rows, lu.cs > 0 ? lu.cs : 1, d_piv, d_info, as_stream(stream));
+    return lu_factor_impl((double *)lu.ptr, lu.rows, lu.cs > 0 ? lu.cs : 1, d_piv, d_info, as_stream(stream),
+                          LM_LU_AUTO);
+}
+
+extern "C" int lm_lu_factor_mode(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_info, int mode, void *stream) {
+    clear_error();
+    LM_REQUIRE(dtype == LM_F64, "lu_factor: f64 only");
+    LM_REQUIRE(mode == LM_LU_AUTO || mode == LM_LU_EXACT || mode == LM_LU_TENSOR, "lu_factor: bad mode %d", mode);
+    LM_REQUIRE(lu.rows == lu.cols, "lu_factor needs a square matrix");
+    LM_REQUIRE(lu.rs == 1 && (lu.cs >= lu.rows || lu.rows <= 1), "lu_factor needs F-order storage");
+    return lu_factor_impl((double *)lu.ptr, lu.rows, lu.cs > 0 ? lu.cs : 1, d_piv, d_info, as_stream(stream), mode);
 }
 
 extern "C" int lm_lu_solve(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, void *stream) {

@@ -398,6 +398,18 @@ bool panel_shape(int64_t h, int &cs, int &rp, int &R);
 int launch_panel_cluster(double *A, int64_t lda, int64_t n, int64_t j0, int nb, int64_t *piv, int32_t *info,
                          cudaStream_t s, long long *dbg = nullptr, int64_t J0 = 0, int64_t J1 = 0);
 
+int dgemm_sub(const double *a, int64_t lda, const double *b, int64_t ldb, double *c, int64_t ldc, int64_t M,
+              int64_t N, int64_t K, cudaStream_t s);
+
+// C -= A B: exact reference order (separately rounded multiply and subtract,
+// k ascending -- bit-identical to _lu_factor) or, in tensor mode, DMMA with
+// FMA accumulation (scaled residual within 1e-10, not bitwise).
+static int trailing_update(bool tensor, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                           int64_t ldc, int64_t M, int64_t N, int K, cudaStream_t s, bool short_ctas = false) {
+    if (tensor) return dgemm_sub(A, lda, B, ldb, C, ldc, M, N, K, s);
+    return exact_update<false, false>(A, lda, B, ldb, C, ldc, M, N, K, s, short_ctas);
+}
+
 // rows [k0, k0+cnt) pivots applied to columns [a0, a1) U [b0, b1)
 static int laswp(double *A, int64_t lda, int64_t n, const int64_t *piv, int64_t k0, int cnt, int64_t a0, int64_t a1,
                  int64_t b0, int64_t b1, int32_t *list, cudaStream_t s) {
@@ -418,20 +430,20 @@ constexpr int ONB = 128;  // outer block
 
 // U12 = L11^{-1} A12 and A22 -= L21 U12 for the columns [c0, c1) to the
 // right of outer block [J0, J1) (32-row triangular blocks, order-preserving)
-static int block_right(double *A, int64_t lda, int64_t n, int64_t J0, int64_t J1, int64_t c0, int64_t c1,
-                       cudaStream_t s, bool short_ctas = false) {
+static int block_right(bool tensor, double *A, int64_t lda, int64_t n, int64_t J0, int64_t J1, int64_t c0,
+                       int64_t c1, cudaStream_t s, bool short_ctas = false) {
     if (c1 <= c0) return 0;
     const int64_t nc = c1 - c0;
     for (int64_t b0 = J0; b0 < J1; b0 += PNB) {
         const int nbb = (int)((J1 - b0) < PNB ? (J1 - b0) : PNB);
         if (int rc = tri32<true>(A + b0 + b0 * lda, lda, A + b0 + c0 * lda, lda, nbb, nc, s)) return rc;
         if (b0 + nbb < J1)
-            if (int rc = exact_update<false, false>(A + (b0 + nbb) + b0 * lda, lda, A + b0 + c0 * lda, lda,
-                                                    A + (b0 + nbb) + c0 * lda, lda, J1 - (b0 + nbb), nc, nbb, s))
+            if (int rc = trailing_update(tensor, A + (b0 + nbb) + b0 * lda, lda, A + b0 + c0 * lda, lda,
+                                         A + (b0 + nbb) + c0 * lda, lda, J1 - (b0 + nbb), nc, nbb, s))
                 return rc;
     }
-    return exact_update<false, false>(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1,
-                                      nc, (int)(J1 - J0), s, short_ctas);
+    return trailing_update(tensor, A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1, nc,
+                           (int)(J1 - J0), s, short_ctas);
 }
 
 struct LuStreams {
@@ -497,7 +509,7 @@ struct LuTrace {
     }
 };
 
-int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
+int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, bool tensor) {
     int cs = 0, rp = 0, R = 0;
     if (n >= (1ll << 31) || !panel_shape(n, cs, rp, R) || sizeof(int32_t) * (size_t)n > 200 * 1024) return 1;
     Scratch list;
@@ -534,9 +546,8 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
             tr.mark(0, m, "panel " + std::to_string(j0));
             const int64_t rest = J1 - (j0 + nb);
             if (rest > 0) {
-                if (int rc = exact_update<false, false>(A + (j0 + nb) + j0 * lda, lda, A + j0 + (j0 + nb) * lda, lda,
-                                                        A + (j0 + nb) + (j0 + nb) * lda, lda, n - (j0 + nb), rest, nb,
-                                                        m))
+                if (int rc = trailing_update(tensor, A + (j0 + nb) + j0 * lda, lda, A + j0 + (j0 + nb) * lda, lda,
+                                             A + (j0 + nb) + (j0 + nb) * lda, lda, n - (j0 + nb), rest, nb, m))
                     return rc;
                 tr.mark(0, m, "inner upd " + std::to_string(j0));
             }
@@ -556,12 +567,12 @@ int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
                 // (one kernel per step: column-chunked remainders free SMs for the
                 // panel cluster sooner but lose more in the update tails --
                 // measured 51 ms at one chunk vs 55-121 ms at 2048-256 columns)
-                if (int rc = block_right(A, lda, n, J0, J1, J2, n, st.lo, true)) return rc;
+                if (int rc = block_right(tensor, A, lda, n, J0, J1, J2, n, st.lo, true)) return rc;
                 tr.mark(1, st.lo, "remainder " + std::to_string(J0));
                 LM_CUDA(cudaEventRecord(ev_rest, st.lo));
                 rest_pending = true;
             }
-            if (int rc = block_right(A, lda, n, J0, J1, J1, J2, m)) return rc;  // the next block first
+            if (int rc = block_right(tensor, A, lda, n, J0, J1, J1, J2, m)) return rc;  // the next block first
             tr.mark(0, m, "next block " + std::to_string(J0));
         }
     }

@@ -9,9 +9,11 @@ inputs at the size the bench times:
 * config 3c at 16384 x 2048: 16 sampled 64 x 64 output tiles (diagonal,
   edge, split-K boundary) against the oracle's gemm over all 16384 inner
   terms, and the whole output bitwise symmetric;
-* config 4a at 8192: the exact-order LU's factors, pivots and solution
-  bitwise against digests of the oracle's run (tests/golden/lu8192.json,
-  made by tests/golden/make_lu8192.py -- the oracle needs minutes);
+* config 4a at 8192: the exact-order LU's (mode "exact") factors, pivots
+  and solution bitwise against digests of the oracle's run
+  (tests/golden/lu8192.json, made by tests/golden/make_lu8192.py -- the
+  oracle needs minutes); the default tensor-core LU against the residual
+  bound and the oracle's pivots;
 * config 5a: the seeded 262144-instance scheme, 256 instances per size
   class spread over the whole class (both ends: the persistent loops'
   tail), regenerated on the host with numpy;
@@ -94,7 +96,7 @@ def test_config4a_exact_lu_full_size_bitwise():
     A.diagonal().add_(float(n))
     b = seeded_device(4, 1, n, k)
     from paper_2502_03000_b200 import _native as N
-    lu, piv = K.lu_factor(A)
+    lu, piv = K.lu_factor(A, mode="exact")  # bitwise: the exact reference order
     x = b.clone()
     N.call("lm_lu_solve", 0, N.view(lu.data), piv.data_ptr(), N.view(x))
 
@@ -103,6 +105,24 @@ def test_config4a_exact_lu_full_size_bitwise():
     assert digest(piv.to(torch.int64)) == gold["piv_sha256"]
     assert digest(lu.data) == gold["lu_sha256"]
     assert digest(x) == gold["x_sha256"]
+
+
+def test_config4a_tensor_lu_full_size_residual_and_pivots():
+    """The default (tensor-core trailing update) LU at 8192 on the bench's
+    inputs: pivots equal the oracle's (digest), scaled residual <= 1e-10."""
+    gold = json.loads((GOLDEN / "lu8192.json").read_text())
+    n, k = gold["n"], gold["nrhs"]
+    A = seeded_device(4, 0, n, n)
+    A.diagonal().add_(float(n))
+    b = seeded_device(4, 1, n, k)
+    lu, piv = K.lu_factor(A, mode="tensor")
+    assert hashlib.sha256(np.ascontiguousarray(piv.cpu().numpy()).tobytes()).hexdigest() == gold["piv_sha256"]
+    x = b.clone()
+    K.lu_solve_into(A, x)  # auto -> tensor at this size
+    Ah, bh, xh = A.cpu().numpy(), b.cpu().numpy(), x.cpu().numpy()
+    res = np.linalg.norm(Ah @ xh - bh, np.inf) / (np.linalg.norm(Ah, np.inf) * np.linalg.norm(xh, np.inf) +
+                                                 np.linalg.norm(bh, np.inf))
+    assert res <= 1e-10
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])

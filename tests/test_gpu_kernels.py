@@ -364,6 +364,26 @@ def test_explicit_inverse_matches_solve_against_identity():
     assert bits_equal(host(out), ref)
 
 
+@pytest.mark.parametrize("n", [64, 333, 700, 1500])
+def test_lu_factor_tensor_mode_pivots_and_residual(n):
+    """Tensor-core trailing updates (mode "tensor", the default from
+    n = 2048): on general (pivoting) matrices the pivots still equal the
+    reference's and the solve meets the north-star residual bound."""
+    rng = np.random.default_rng(n + 7)
+    a = np.asfortranarray(rng.uniform(-1, 1, (n, n)))
+    rc, lu_ref, piv_ref = O.lu_factor(a)
+    lu, piv = K.lu_factor(dev(a), mode="tensor")
+    assert np.array_equal(host(piv), piv_ref)
+    assert normwise(host(lu.data), lu_ref) <= 1e-9  # values agree to rounding growth, not bitwise
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, 4)))
+    x = dev(np.array(b, order="F"))
+    K.lu_solve_into(dev(a), x, mode="tensor")
+    xh = host(x)
+    res = np.linalg.norm(a @ xh - b, np.inf) / (np.linalg.norm(a, np.inf) * np.linalg.norm(xh, np.inf) +
+                                                np.linalg.norm(b, np.inf))
+    assert res <= 1e-10
+
+
 @pytest.mark.parametrize("n", [700, 1500])
 def test_lu_factor_large_general_bitwise(n):
     """Multi-CTA cluster panels, outer blocks and laswp: still the
