@@ -180,6 +180,25 @@ int lm_analyze_batched(int dtype, int64_t n, int64_t batch, const void *a, int64
 int lm_expr_atb_schur_trace_batched(int dtype, int64_t n, int64_t batch, const void *a, const void *b,
                                     const void *c, const void *d, void *e, void *s, void *stream);
 
+/* ---- the collective of the row-sharded configs ---- */
+/* NCCL is resolved at run time: `path` (or NULL) names the library; the copy
+ * already loaded in the process (torch's) is preferred.  One process per
+ * GPU: rank 0 makes the 128-byte unique id, the host layer moves it to the
+ * other ranks (any rendezvous), every rank calls lm_nccl_init_rank on its
+ * device.  lm_nccl_init_all is the single-process, several-device form
+ * (ncclCommInitAll; comms_out receives ndev communicators).  Returns -3 on an
+ * NCCL error (lm_last_error() explains). */
+#define LM_NCCL_ID_BYTES 128
+int lm_nccl_load(const char *path, int *version_out);
+int lm_nccl_unique_id(uint8_t *id_out);
+int lm_nccl_init_rank(int nranks, int rank, const uint8_t *id, void **comm_out);
+int lm_nccl_init_all(int ndev, const int *devs, void **comms_out);
+/* In-place sum all-reduce of `count` elements on `stream` (asynchronous). */
+int lm_allreduce_sum(void *comm, int dtype, void *d_buf, int64_t count, void *stream);
+/* The 5b trace finish: one float64 (lazymat/kernels.py:157-164 per shard). */
+int lm_allreduce_sum_f64(void *comm, double *d_val, void *stream);
+int lm_nccl_destroy(void *comm);
+
 /* ---- synthetic data (bench / tests only) ------------------------------- */
 /* out(i,j) = U(lo,hi) from a counter-based hash of the GLOBAL index
  * (row0+i, col0+j) of a matrix with global_rows rows: any slice of a

@@ -35,7 +35,8 @@ EXPORTS = (
     "lm_analyze", "lm_lu_factor", "lm_lu_factor_mode", "lm_lu_solve", "lm_band_solve", "lm_tri_solve",
     "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
     "lm_lu_solve_batched", "lm_solve_batched_classified", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
-    "lm_fill_pcg64",
+    "lm_fill_pcg64", "lm_nccl_load", "lm_nccl_unique_id", "lm_nccl_init_rank", "lm_nccl_init_all",
+    "lm_allreduce_sum", "lm_allreduce_sum_f64", "lm_nccl_destroy",
     "lm_debug_lu_panel",
 )
 
@@ -83,6 +84,13 @@ _SIGS = {
     "lm_fill_uniform": (_i, [_i, View, ctypes.c_uint64, _i64, _i64, _i64, _d, _d, _p]),
     "lm_fill_pcg64": (_i, [_i, _p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_uint64, ctypes.c_uint64,
                            ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, _d, _d, _p]),
+    "lm_nccl_load": (_i, [ctypes.c_char_p, ctypes.POINTER(_i)]),
+    "lm_nccl_unique_id": (_i, [ctypes.c_char_p]),
+    "lm_nccl_init_rank": (_i, [_i, _i, ctypes.c_char_p, ctypes.POINTER(_p)]),
+    "lm_nccl_init_all": (_i, [_i, ctypes.POINTER(_i), ctypes.POINTER(_p)]),
+    "lm_allreduce_sum": (_i, [_p, _i, _p, _i64, _p]),
+    "lm_allreduce_sum_f64": (_i, [_p, _p, _p]),
+    "lm_nccl_destroy": (_i, [_p]),
     "lm_debug_lu_panel": (_i, [View, _i64, _i, _p, _p, _p, _p]),
 }
 

@@ -29,9 +29,20 @@ CUDA_HOME = pathlib.Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_include():
+    """nccl.h of the NCCL torch ships (the library is dlopen'ed at run time)."""
+    for site in sys.path:
+        inc = pathlib.Path(site) / "nvidia" / "nccl" / "include"
+        if (inc / "nccl.h").exists():
+            return [f"-I{inc}"]
+    return []
+
+
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
                      "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills", f"-I{INCLUDE}", f"-I{CSRC}",
-                     "-cudart", "shared"]
+                     "-cudart", "shared"] + _nccl_include()
 
 
 def sources():
@@ -73,7 +84,7 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     if force or _needs(LIB, objs):
         tmp = LIB.with_suffix(f".so.{os.getpid()}.tmp")
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", str(tmp), *map(str, objs),
-               f"-L{CUDA_HOME / 'lib64'}", "-lnvrtc", "-Xlinker", f"-rpath,{CUDA_HOME / 'lib64'}"]
+               f"-L{CUDA_HOME / 'lib64'}", "-lnvrtc", "-ldl", "-Xlinker", f"-rpath,{CUDA_HOME / 'lib64'}"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -12,21 +12,27 @@ operand (``row_range``: contiguous, balanced):
   partial with the same trace_of_product kernel (it accepts p x q / q x p
   operands, lazymat/kernels.py:157-164), and one NCCL all-reduce of a
   single float64 finishes it -- the only collective, because it is the
-  only real exchange step.
+  only real exchange step.  The all-reduce goes through
+  the C-ABI (lm_allreduce_sum_f64 on an lm_nccl_init_rank communicator,
+  ``NcclComm``); torch.distributed only carries the 128-byte NCCL unique id
+  from rank 0 to the others.
 
 The partial-trace function is injectable so the host-side sharding and
 reduction logic is testable on CPU with the gloo backend
-(tests/test_shard.py); the product path always uses the CUDA kernel.
+(tests/test_shard.py: CPU tensors reduce through torch.distributed there);
+the product path always uses the CUDA kernel and the library's NCCL.
 """
 
 from __future__ import annotations
+
+import ctypes
 
 import torch
 
 from . import kernels
 from .matrix import DenseMatrix
 
-__all__ = ["row_range", "ShardedTrace", "eval_rows", "fill_uniform", "partition_by_cost", "class_ranges"]
+__all__ = ["row_range", "ShardedTrace", "NcclComm", "eval_rows", "fill_uniform", "partition_by_cost", "class_ranges"]
 
 
 def row_range(n: int, rank: int, world: int) -> tuple:
@@ -79,12 +85,64 @@ def _device_partial(a_rows: torch.Tensor, b_cols: torch.Tensor, out: torch.Tenso
     kernels.trace_of_product(a_rows, b_cols, out=out)
 
 
+def _dist_world(group=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+class NcclComm:
+    """An NCCL communicator of the C-ABI (lm_nccl_init_rank), one process
+    per GPU.  Rank 0 creates the unique id; with more than one rank it is
+    broadcast over torch.distributed (rendezvous only -- no tensor data).
+    Create it on every rank with the rank's device current."""
+
+    def __init__(self, group=None):
+        from . import _native as N
+        self._N = N
+        lib = N.load_library()
+        self.rank, self.world = _dist_world(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            N.check(lib.lm_nccl_unique_id(uid), "lm_nccl_unique_id")
+        if self.world > 1:
+            import torch.distributed as dist
+            box = [uid.raw if self.rank == 0 else None]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        self._comm = ctypes.c_void_p()
+        N.check(lib.lm_nccl_init_rank(self.world, self.rank, uid, ctypes.byref(self._comm)), "lm_nccl_init_rank")
+
+    def allreduce_sum(self, t: torch.Tensor) -> torch.Tensor:
+        """In-place sum over the ranks, asynchronous on the current stream."""
+        N = self._N
+        N._dev_check(t)
+        if not t.is_contiguous():
+            raise ValueError("allreduce_sum: contiguous tensor expected")
+        N.call("lm_allreduce_sum", self._comm, N.dtype_code(t), t.data_ptr(), t.numel())
+        return t
+
+    def close(self):
+        if self._comm:
+            self._N.check(self._N.load_library(False).lm_nccl_destroy(self._comm), "lm_nccl_destroy")
+            self._comm = ctypes.c_void_p()
+
+    def __del__(self):  # best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class ShardedTrace:
     """trace(A @ B) over row shards: local partial + one all-reduce."""
 
-    def __init__(self, group=None, partial_fn=None):
+    def __init__(self, group=None, partial_fn=None, comm: "NcclComm | None" = None):
         self.group = group
         self.partial_fn = partial_fn or _device_partial
+        self.comm = comm
 
     def __call__(self, a_rows: torch.Tensor, b_cols: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
         """a_rows: (R, n) row block of A; b_cols: (n, R) matching column
@@ -93,8 +151,12 @@ class ShardedTrace:
         if out is None:
             out = torch.empty(1, dtype=a_rows.dtype, device=a_rows.device)
         self.partial_fn(a_rows, b_cols, out)
-        import torch.distributed as dist
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+        if out.is_cuda:
+            if self.comm is None:  # created on first use, on every rank (collective rendezvous)
+                self.comm = NcclComm(self.group)
+            self.comm.allreduce_sum(out)
+        elif _dist_world(self.group)[1] > 1:
+            import torch.distributed as dist  # CPU partials (the gloo test of the sharding logic)
             dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
         return out
 

@@ -180,3 +180,22 @@ def test_config5b_row_block_world1():
     s = ShardedTrace()(blk[0], bc)
     tr = O.trace_of_product(np.asfortranarray(h[0]), np.asfortranarray(bch))
     assert abs(float(s.item()) - tr) <= 1e-12 * abs(tr)
+
+
+def test_nccl_allreduce_through_the_c_abi_world1():
+    """The 5b finish: lm_nccl_init_rank + lm_allreduce_sum_f64 (world size 1:
+    the sum over one rank is the identity, but the NCCL calls run)."""
+    import ctypes
+    from paper_2502_03000_b200 import _native as N
+    from paper_2502_03000_b200.shard import NcclComm
+    ver = ctypes.c_int(0)
+    N.check(N.load_library().lm_nccl_load(None, ctypes.byref(ver)), "lm_nccl_load")
+    assert ver.value >= 22700
+    comm = NcclComm()
+    t = torch.tensor([3.25, -1.5], dtype=torch.float64, device="cuda")
+    comm.allreduce_sum(t)
+    assert t.cpu().tolist() == [3.25, -1.5]
+    s = torch.tensor([2.0], dtype=torch.float64, device="cuda")
+    N.call("lm_allreduce_sum_f64", comm._comm, s.data_ptr())
+    assert float(s.item()) == 2.0
+    comm.close()
