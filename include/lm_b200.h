@@ -102,6 +102,11 @@ int lm_vec_sum(int dtype, lm_vec v, void *d_result, void *stream);
 /* out = a @ b (a p x q, b q x r).  r == 1 or p == 1 dispatch to the
  * split-K GEMV kernel; otherwise the FP64 DMMA tensor-core GEMM. */
 int lm_gemm(int dtype, lm_view a, lm_view b, lm_view out, void *stream);
+/* out = x @ (y @ z) and t = y @ z in ONE cooperative launch (the R6 plan of
+ * a shape-skewed chain: two consecutive _gemm steps, _loops.py:87-98) when
+ * t is at most 128 x 128 and dtype is f64: returns 1 (nothing launched) for
+ * other shapes, so the caller runs the two lm_gemm calls instead. */
+int lm_gemm_chain(int dtype, lm_view x, lm_view y, lm_view z, lm_view t, lm_view out, void *stream);
 /* out = a @ x (trans=0) or a.T @ x (trans=1) (kernels.py:88-103). */
 int lm_gemv(int dtype, lm_view a, lm_vec x, lm_vec out, int trans, void *stream);
 /* out = a @ a.T, upper triangle computed, lower mirrored bitwise. */

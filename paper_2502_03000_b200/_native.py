@@ -30,7 +30,7 @@ LU_MODES = {"auto": 0, "exact": 1, "tensor": 2}  # lm_lu_factor_mode (include/lm
 EXPORTS = (
     "lm_abi_version", "lm_last_error", "lm_launch_count", "lm_last_variant",
     "lm_fused_axpby", "lm_fused_program", "lm_program_source", "lm_copy", "lm_vec_sum",
-    "lm_gemm", "lm_gemv", "lm_syrk",
+    "lm_gemm", "lm_gemm_chain", "lm_gemv", "lm_syrk",
     "lm_diag_scale", "lm_diag_of_product", "lm_trace_of_product", "lm_triple_diag_dot",
     "lm_analyze", "lm_lu_factor", "lm_lu_factor_mode", "lm_lu_solve", "lm_band_solve", "lm_tri_solve",
     "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
@@ -62,6 +62,7 @@ _SIGS = {
     "lm_copy": (_i, [_i, View, View, _p]),
     "lm_vec_sum": (_i, [_i, Vec, _p, _p]),
     "lm_gemm": (_i, [_i, View, View, View, _p]),
+    "lm_gemm_chain": (_i, [_i, View, View, View, View, View, _p]),
     "lm_gemv": (_i, [_i, View, Vec, Vec, _i, _p]),
     "lm_syrk": (_i, [_i, View, View, _p]),
     "lm_diag_scale": (_i, [_i, Vec, View, _i, View, _p]),

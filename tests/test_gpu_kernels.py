@@ -439,3 +439,45 @@ def test_config4a_full_size_residual_and_pivots():
     assert resid <= bound
     _, piv = K.lu_factor(A.data)
     assert np.array_equal(host(piv), np.arange(n))  # dominant diagonal: the reference never swaps
+
+
+@pytest.mark.parametrize("m,p,k,q", [(8000, 100, 8000, 100), (37, 5, 1000, 7), (1, 1, 3, 1), (300, 128, 129, 128),
+                                     (10000, 64, 40, 33)])
+def test_gemm_chain_fused_vs_oracle(m, p, k, q):
+    """lm_gemm_chain (one cooperative launch: split-K Y Z, fixed-order
+    finish, X T) against the oracle's two _gemm calls; run-to-run bitwise."""
+    rng = np.random.default_rng(m + p + k + q)
+    X = np.asfortranarray(rng.uniform(-1, 1, (m, p)))
+    Y = np.asfortranarray(rng.uniform(-1, 1, (p, k)))
+    Z = np.asfortranarray(rng.uniform(-1, 1, (k, q)))
+    T_ref = np.zeros((p, q), order="F")
+    O.gemm(Y, Z, T_ref)
+    ref = np.zeros((m, q), order="F")
+    O.gemm(X, T_ref, ref)
+    t, out = fortran_empty(p, q, device=DEV), fortran_empty(m, q, device=DEV)
+    K.gemm_chain_launch(dev(X), dev(Y), dev(Z), t, out)
+    assert normwise(host(t), T_ref) <= 1e-12
+    assert normwise(host(out), ref) <= 1e-12
+    again = fortran_empty(m, q, device=DEV)
+    K.gemm_chain_launch(dev(X), dev(Y), dev(Z), t, again)
+    assert torch.equal(out, again)
+
+
+def test_chain_plan_fused_with_identical_events(monkeypatch):
+    """X*Y*Z through evaluate() with the chain fusion on (LM_GEMM_CHAIN=1):
+    the executor fuses the two gemm steps into one launch but records exactly
+    the events of the two-step plan."""
+    from paper_2502_03000_b200 import rewrite as rw
+    monkeypatch.setattr(rw, "_CHAIN_ON", True)
+    rng = np.random.default_rng(3)
+    X, Y, Z = (lm.DenseMatrix(np.asfortranarray(rng.uniform(-1, 1, s))) for s in ((500, 40), (40, 700), (700, 40)))
+    plan = lm.rewrite(X * Y * Z)
+    assert [s.kernel for s in plan.steps] == ["gemm", "gemm"]
+    from paper_2502_03000_b200 import _native
+    c0 = _native.launch_count()
+    tr = lm.with_trace(lambda: lm.evaluate(X * Y * Z))
+    assert _native.launch_count() - c0 == 1  # one cooperative kernel
+    kinds = [e.kind for e in tr.events]
+    assert kinds.count("kernel") == 2 and [e.name for e in tr.events if e.kind == "kernel"] == ["gemm", "gemm"]
+    ref = X.to_numpy() @ (Y.to_numpy() @ Z.to_numpy())
+    assert normwise(tr.result.to_numpy(), ref) <= 1e-12

@@ -1,1 +1,1 @@
-timeout 300 python tools/small_lu_probe.py
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x -k "chain or gemm" 2>&1 | tail -2
