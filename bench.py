@@ -1374,6 +1374,8 @@ def run_ours(args, wl, ws, rank, local):
             achieved, unit = work / (kms * 1e-3) / 1e9, "GB/s"
             if kflops is not None:
                 fpeak, fkind = _fp64_peak() if wl.dtype == "f64" else _tf32x3_peak()
+                if getattr(wl, "exact_fp64", False):
+                    fpeak, fkind = fpeak / 2, fkind + "; /2 for exact mul+sub (no FMA)"
                 fach = kflops / (kms * 1e-3) / 1e12
                 if fach / fpeak > achieved / peak:  # the kernel is compute-bound: report that roofline
                     work, achieved, peak, peak_kind, unit = kflops, fach, fpeak, fkind, "TFLOP/s"

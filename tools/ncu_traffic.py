@@ -33,7 +33,8 @@ def run(config, order_path):
     thunks = wl.kernels_for_roofline(lm, ctx)
     torch.cuda.synchronize()
     c0 = N.launch_count()
-    for name, work, thunk in thunks:
+    for entry in thunks:
+        name, work, thunk = entry[:3]
         thunk()
         torch.cuda.synchronize()
         c1 = N.launch_count()
@@ -52,12 +53,17 @@ def merge(config, csv_path, order_path):
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hdr]
     ik, im, iv, iid = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
+    iu = h.index("Metric Unit") if "Metric Unit" in h else None
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     launches = {}
     for r in rows[hdr + 1:]:
         if len(r) <= iv:
             continue
         d = launches.setdefault(int(r[iid]), {"name": r[ik]})
-        d[r[im]] = float(r[iv].replace(",", ""))
+        v = float(r[iv].replace(",", ""))
+        if iu is not None and r[im].startswith("dram__bytes"):
+            v *= scale.get(r[iu], 1.0)
+        d[r[im]] = v
     seq = [launches[k] for k in sorted(launches)]
     meta = json.loads(pathlib.Path(order_path).read_text())
     base = len(seq) - meta["total"]
