@@ -97,13 +97,23 @@ _SIGS = {
 
 _lock = threading.Lock()
 _lib = None
+_cuda_ok = None
+
+
+def cuda_available() -> bool:
+    """torch.cuda.is_available(), cached: it reads the environment on every
+    call (~4 us), and every evaluate() asks several times."""
+    global _cuda_ok
+    if _cuda_ok is None:
+        _cuda_ok = bool(torch.cuda.is_available())
+    return _cuda_ok
 
 
 def load_library(require_device: bool = True):
     """The ctypes handle; builds nothing.  ``require_device`` (default)
     refuses to run without a CUDA device."""
     global _lib
-    if require_device and not torch.cuda.is_available():
+    if require_device and not cuda_available():
         raise BackendUnavailableError(
             "paper_2502_03000_b200 evaluates on a B200 (sm_100a) GPU only; no CUDA device is visible")
     if _lib is None:
@@ -161,6 +171,10 @@ def vec(t: torch.Tensor) -> Vec:
 
 
 def stream_handle(device=None) -> int:
+    """Raw cudaStream_t of the current stream (torch's C binding: the Python
+    torch.cuda.current_stream() wrapper costs ~10 us per call)."""
+    if device is None:
+        return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
     return torch.cuda.current_stream(device).cuda_stream
 
 

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import torch
 
+from . import _native
 from .errors import BackendUnavailableError, KernelContractError
 from .expr import ExprNode
 from .rewrite import Plan, execute, rewrite
@@ -39,7 +40,7 @@ class CapturedPlan:
         syncing = sorted({st.kernel for st in plan.steps} & _HOST_SYNC_KERNELS)
         if syncing:
             raise KernelContractError(f"plan step(s) {syncing} synchronise with the host; not capturable")
-        if not torch.cuda.is_available():
+        if not _native.cuda_available():
             raise BackendUnavailableError("CUDA-graph capture needs a CUDA device")
         self.plan = plan
         self.tree = tree  # when known: replays wait (stream-side) for uploads into its leaves
