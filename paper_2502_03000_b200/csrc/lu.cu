@@ -346,6 +346,7 @@ int launch_trsm(const double *T, int64_t ldt, double *X, int64_t ldx, int nbj, i
 constexpr int kLuNb = 64;
 
 int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, bool tensor);
+int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s);
 int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s);
 template <bool DESC, bool SKIP_ZERO>
 int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
@@ -378,7 +379,12 @@ int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
     // two-level blocked LU with a thread-block-cluster panel (lu_fast.cu);
     // returns 1 when the panel does not fit a cluster -> cooperative path
     // (exact order only)
-    if (int rc = lu_factor_fast(A, n, lda, piv, info, s, lu_tensor_mode(mode, n)); rc != 1) return rc;
+    const bool tensor = lu_tensor_mode(mode, n);
+    // tensor mode, column diagonally dominant A: partial pivoting provably
+    // never swaps -> the pivot-free, all-GEMM factorisation (lu_nopiv.cu)
+    if (tensor)
+        if (int rc = lu_factor_nopiv(A, n, lda, piv, info, s); rc != 1) return rc;
+    if (int rc = lu_factor_fast(A, n, lda, piv, info, s, tensor); rc != 1) return rc;
     const int nsm = num_sms();
     Scratch pub;
     const int maxP = nsm;

@@ -1,0 +1,365 @@
+// lu_nopiv.cu -- the blocked LU when partial pivoting provably never swaps.
+//
+// If A is strictly diagonally dominant by columns (|a_jj| > sum_{i != j}
+// |a_ij| for every j), Gaussian elimination with partial pivoting performs
+// no row interchanges: the diagonal entry is the unique maximum of its
+// column, and every Schur complement stays column diagonally dominant
+// (Golub & Van Loan, "Matrix Computations", diagonal dominance and GEPP).
+// The reference's _lu_factor (lazymat/_loops.py:200-236) would therefore
+// choose pivot k at every step; config 4a's A = U(-1,1) + 8192 I is such a
+// matrix.  In tensor mode (values at residual level, pivots exact) the LU
+// then needs no pivot search at all, and every step is GEMM-shaped:
+//
+//   per 64-column block J (right-looking, look-ahead of one block):
+//     hi stream  diag_nopiv: A11 = L11 U11 in one CTA (shared memory), plus
+//                L11^-1 and U11^-1 (column-parallel substitution);
+//                L21 = A21 U11^-1 (DMMA GEMM), U12 of the NEXT block's
+//                columns = L11^-1 A12, and that column panel's update
+//     lo stream  U12 of the remaining columns, A22 -= L21 U12 (DMMA, the
+//                bulk of the 2n^3/3 flops)
+//
+// The dominance test runs first (one pass over A, with a margin far above
+// rounding so the reference's own rounded Schur complements keep the same
+// strict maxima), and after the factorisation every multiplier is checked
+// to be strictly inside (-1, 1) by the same margin (lower_absmax); if that
+// ever failed, the original matrix (kept in a backup) is factored again by
+// the pivoting path.  Pivots come back as the identity -- exactly what the
+// reference computes for these matrices.
+#include <chrono>
+#include <cstdlib>
+#include <vector>
+
+#include "common.cuh"
+
+namespace lm {
+
+int dgemm(const double *a, int64_t a_sm, int64_t a_sk, const double *b, int64_t b_sk, int64_t b_sn, double *c,
+          int64_t c_sm, int64_t c_sn, int64_t M, int64_t N, int64_t K, bool syrk, cudaStream_t s);
+int dgemm_sub(const double *a, int64_t lda, const double *b, int64_t ldb, double *c, int64_t ldc, int64_t M,
+              int64_t N, int64_t K, cudaStream_t s);
+
+namespace {
+
+constexpr int NBD = 64;          // block width
+constexpr int LDD = NBD + 1;     // shared-memory column length (odd: conflict-free column walks)
+constexpr double kDomMargin = 1.001;   // |a_jj| > kDomMargin * sum_{i != j} |a_ij|
+constexpr double kMulBound = 0.999;    // every multiplier |l_ij| < kMulBound (then the argmax is strict)
+
+// one warp per column: flag columns that are not strictly dominant (or hold NaN / Inf)
+__global__ void __launch_bounds__(256) coldom_check(const double *__restrict__ A, int64_t n, int64_t lda,
+                                                   int *__restrict__ flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = w; j < n; j += nw) {
+        const double *col = A + j * lda;
+        double s = 0.0;
+        for (int64_t i = lane; i < n; i += 32)
+            if (i != j) s += fabs(col[i]);
+        s = warp_sum(s);
+        if (lane == 0) {
+            const double d = fabs(col[j]);
+            if (!(d > kDomMargin * s) || !(s < 1e300)) atomicOr(flag, 1);
+        }
+    }
+}
+
+// A11 = L11 U11 (no pivoting) of the nb x nb block at A (nb <= NBD), in
+// shared memory, FMA arithmetic (tensor mode); 512 threads on a 2-D map (row
+// lane tx, column slice ty), one barrier pair per column.
+__global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb) {
+    __shared__ double a[NBD * LDD];  // (i, j) at a[j * LDD + i]
+    const int tid = threadIdx.x;
+    const int tx = tid & (NBD - 1), ty = tid >> 6;
+    for (int c = ty; c < nb; c += 8)
+        if (tx < nb) a[c * LDD + tx] = A[tx + (int64_t)c * lda];
+    __syncthreads();
+    for (int k = 0; k < nb; ++k) {
+        const double p = a[k * LDD + k];
+        if (ty == 0 && tx > k && tx < nb) a[k * LDD + tx] /= p;  // multipliers l_ik
+        __syncthreads();
+        if (tx > k && tx < nb) {
+            const double l = a[k * LDD + tx];
+            for (int c = k + 1 + ty; c < nb; c += 8) a[c * LDD + tx] = fma(-l, a[c * LDD + k], a[c * LDD + tx]);
+        }
+        __syncthreads();
+    }
+    for (int c = ty; c < nb; c += 8)
+        if (tx < nb) A[tx + (int64_t)c * lda] = a[c * LDD + tx];
+}
+
+// L21 = A21 U11^-1 in place: one thread per row of A21 (rows [0, M) at
+// A21, leading dimension lda), the row in registers (static indices: the
+// substitution is unrolled over the block width), U11 (nb x nb at U) in
+// shared memory.  Row-wise forward substitution x U = a:
+//   for i: x_i = s_i / u_ii; s_j -= x_i u_ij (j > i)
+__global__ void __launch_bounds__(128) trsm_right_upper(double *A21, int64_t lda, int64_t M, const double *U,
+                                                       int nb) {
+    __shared__ double u[NBD * LDD];  // (i, j) at u[j * LDD + i]
+    for (int e = threadIdx.x; e < NBD * NBD; e += blockDim.x) {
+        const int i = e & (NBD - 1), j = e >> 6;
+        u[j * LDD + i] = (i < nb && j < nb) ? U[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+    }
+    __syncthreads();
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= M) return;
+    double s[NBD];
+#pragma unroll
+    for (int c = 0; c < NBD; ++c) s[c] = c < nb ? A21[r + c * lda] : 0.0;
+#pragma unroll
+    for (int i = 0; i < NBD; ++i) {
+        const double x = s[i] / u[i * LDD + i];
+        s[i] = x;
+#pragma unroll
+        for (int j = i + 1; j < NBD; ++j) s[j] = fma(-x, u[j * LDD + i], s[j]);
+    }
+#pragma unroll
+    for (int c = 0; c < NBD; ++c)
+        if (c < nb) A21[r + c * lda] = s[c];
+}
+
+// U12 = L11^-1 A12 in place: one thread per column of A12 (nb rows, columns
+// [0, N) at A12), unit lower L11 (at L) in shared memory.
+//   for k: y_k final; y_i -= l_ik y_k (i > k)
+__global__ void __launch_bounds__(128) trsm_left_lower_unit(double *A12, int64_t lda, int64_t N, const double *L,
+                                                           int nb) {
+    __shared__ double l[NBD * LDD];  // (i, k) at l[k * LDD + i]
+    for (int e = threadIdx.x; e < NBD * NBD; e += blockDim.x) {
+        const int i = e & (NBD - 1), k = e >> 6;
+        l[k * LDD + i] = (i < nb && k < nb && i > k) ? L[i + (int64_t)k * lda] : 0.0;
+    }
+    __syncthreads();
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= N) return;
+    double y[NBD];
+    double *col = A12 + c * lda;
+#pragma unroll
+    for (int i = 0; i < NBD; ++i) y[i] = i < nb ? col[i] : 0.0;
+#pragma unroll
+    for (int k = 0; k < NBD; ++k)
+#pragma unroll
+        for (int i = k + 1; i < NBD; ++i) y[i] = fma(-l[k * LDD + i], y[k], y[i]);
+#pragma unroll
+    for (int i = 0; i < NBD; ++i)
+        if (i < nb) col[i] = y[i];
+}
+
+// max |l_ij| over the strictly lower triangle of the n x n factor (bit pattern
+// of a non-negative double orders like the value)
+__global__ void __launch_bounds__(256) lower_absmax(const double *__restrict__ A, int64_t n, int64_t lda,
+                                                   unsigned long long *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double m = 0.0;
+    for (int64_t j = w; j < n; j += nw)
+        for (int64_t i = j + 1 + lane; i < n; i += 32) {
+            const double v = fabs(A[i + j * lda]);
+            m = v > m || v != v ? (v != v ? 1e300 : v) : m;
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void iota_piv(int64_t *piv, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        piv[i] = i;
+}
+
+struct NoPivStreams {
+    cudaStream_t hi = nullptr, lo = nullptr;
+};
+
+int nopiv_streams(NoPivStreams &st) {
+    static PerDevice<NoPivStreams> cache;
+    return cache.get(st, [](NoPivStreams &c) {
+        int least = 0, greatest = 0;
+        LM_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        LM_CUDA(cudaStreamCreateWithPriority(&c.hi, cudaStreamNonBlocking, greatest));
+        LM_CUDA(cudaStreamCreateWithPriority(&c.lo, cudaStreamNonBlocking, least));
+        return 0;
+    });
+}
+
+// The factorisation proper (A is known column-dominant).  Asynchronous on s.
+int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
+    NoPivStreams st;
+    if (int rc = nopiv_streams(st)) return rc;
+    cudaEvent_t ev_fork, ev_l21, ev_rest, ev_join;
+    LM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_l21, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    struct EvGuard {
+        cudaEvent_t e[4];
+        ~EvGuard() {
+            for (auto x : e) cudaEventDestroy(x);
+        }
+    } guard{{ev_fork, ev_l21, ev_rest, ev_join}};
+    LM_CUDA(cudaEventRecord(ev_fork, s));
+    LM_CUDA(cudaStreamWaitEvent(st.hi, ev_fork, 0));
+    LM_CUDA(cudaStreamWaitEvent(st.lo, ev_fork, 0));
+    // Look-ahead of one block.  Block J's trailing update on lo (columns
+    // J2..n) overlaps block J+1's diagonal factor and L21 on hi; hi waits for
+    // it only before touching those columns (block J+1's U12 of the next
+    // panel and that panel's update).
+    // LM_NOPIV_TRACE=1: per-phase device time on each stream (stderr)
+    static const bool trace = getenv("LM_NOPIV_TRACE") != nullptr;
+    std::vector<cudaEvent_t> evs;
+    std::vector<int> tags;  // 0 diag, 1 L21, 2 next panel, 3 rest (lo)
+    auto mark = [&](cudaStream_t str, int tag) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, str);
+        evs.push_back(e);
+        tags.push_back(tag);
+    };
+    const auto h0 = std::chrono::steady_clock::now();
+    mark(st.hi, -1);
+    mark(st.lo, -2);
+    // Outer blocks of OB = 2 x 64 columns (rank-128 trailing updates: the DMMA
+    // GEMM runs at ~32 TF/s at K = 128, ~12 at K = 64), each factored as two
+    // 64-column inner blocks a, b.
+    constexpr int OB = 2 * NBD;
+    auto trsm_ru = [&](double *A21, int64_t M, const double *U, int nb, cudaStream_t str) -> int {
+        if (M <= 0) return 0;
+        trsm_right_upper<<<(unsigned)ceil_div(M, 64), 64, 0, str>>>(A21, lda, M, U, nb);
+        LM_LAUNCHED(1);
+        return 0;
+    };
+    auto trsm_ll = [&](double *A12, int64_t N, const double *L, int nb, cudaStream_t str) -> int {
+        if (N <= 0) return 0;
+        trsm_left_lower_unit<<<(unsigned)ceil_div(N, 64), 64, 0, str>>>(A12, lda, N, L, nb);
+        LM_LAUNCHED(1);
+        return 0;
+    };
+    bool rest_pending = false;
+    for (int64_t J0 = 0; J0 < n; J0 += OB) {
+        const int na = (int)((n - J0) < NBD ? (n - J0) : NBD);
+        const int64_t Ja = J0 + na;
+        const int nbb = (int)((n - Ja) < NBD ? (n - Ja) : NBD);  // 0 at the very end
+        const int64_t J1 = Ja + nbb, J2 = (J1 + OB) < n ? J1 + OB : n;
+        const int nob = (int)(J1 - J0);
+        double *Aaa = A + J0 + J0 * lda, *Abb = A + Ja + Ja * lda;
+        // ---- factor the outer panel (columns J0..J1, rows J0..n) on hi
+        diag_nopiv<<<1, 512, 0, st.hi>>>(Aaa, lda, na);
+        LM_LAUNCHED(1);
+        mark(st.hi, 0);
+        if (int rc = trsm_ru(A + Ja + J0 * lda, n - Ja, Aaa, na, st.hi)) return rc;  // L of block a, rows below a
+        if (nbb > 0) {
+            if (int rc = trsm_ll(A + J0 + Ja * lda, nbb, Aaa, na, st.hi)) return rc;  // U_ab
+            if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + Ja * lda, lda, Abb, lda, n - Ja, nbb, na, st.hi))
+                return rc;
+            diag_nopiv<<<1, 512, 0, st.hi>>>(Abb, lda, nbb);
+            LM_LAUNCHED(1);
+            if (int rc = trsm_ru(A + J1 + Ja * lda, n - J1, Abb, nbb, st.hi)) return rc;  // L of block b
+        }
+        LM_CUDA(cudaEventRecord(ev_l21, st.hi));
+        mark(st.hi, 1);
+        if (J1 >= n) break;
+        // ---- U12 of the outer block's rows over the columns [c0, c0 + nc), then
+        // the rank-nob update of the rows below
+        auto u12 = [&](int64_t c0, int64_t nc, cudaStream_t str) -> int {
+            if (int rc = trsm_ll(A + J0 + c0 * lda, nc, Aaa, na, str)) return rc;
+            if (nbb > 0) {
+                if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + c0 * lda, lda, A + Ja + c0 * lda, lda, nbb, nc,
+                                       na, str))
+                    return rc;
+                if (int rc = trsm_ll(A + Ja + c0 * lda, nc, Abb, nbb, str)) return rc;
+            }
+            return dgemm_sub(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1, nc, nob,
+                             str);
+        };
+        // the remaining columns on the low-priority stream (after the previous
+        // outer block's, which wrote the same columns)
+        const int64_t nn2 = n - J2;
+        if (nn2 > 0) {
+            LM_CUDA(cudaStreamWaitEvent(st.lo, ev_l21, 0));
+            if (int rc = u12(J2, nn2, st.lo)) return rc;
+            mark(st.lo, 3);
+        }
+        // the next outer panel's columns were last written by the previous
+        // block's trailing update: wait for it, then their U12 and update
+        if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
+        if (int rc = u12(J1, J2 - J1, st.hi)) return rc;
+        mark(st.hi, 2);
+        rest_pending = nn2 > 0;
+        if (rest_pending) LM_CUDA(cudaEventRecord(ev_rest, st.lo));
+    }
+    if (trace) {
+        const double host_us =
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
+        cudaDeviceSynchronize();
+        double tot[4] = {0, 0, 0, 0}, last_hi = 0, last_lo = 0;
+        float t;
+        for (size_t i = 2; i < evs.size(); ++i) {
+            const bool lo = tags[i] == 3;
+            cudaEventElapsedTime(&t, evs[0], evs[i]);
+            double &last = lo ? last_lo : last_hi;
+            tot[tags[i]] += t - last;
+            last = t;
+        }
+        fprintf(stderr, "NOPIVTRACE host issue %.0f us | hi: diag %.2f ms, L21 %.2f ms, next panel (incl. wait) %.2f ms, "
+                        "end %.2f ms | lo: rest end %.2f ms (busy %.2f)\n",
+                host_us, tot[0], tot[1], tot[2], last_hi, last_lo, tot[3]);
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+    if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
+    LM_CUDA(cudaEventRecord(ev_join, st.hi));
+    LM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    return 0;
+}
+
+}  // namespace
+
+bool lu_nopiv_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LM_LU_NOPIV");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// 0: factored without swaps (piv = identity, *info = 0); 1: not applicable
+// (A is not column-dominant, or a multiplier came out too close to 1 and A
+// was restored) -- the caller runs the pivoting LU; < 0: error.
+// Synchronises s twice (the dominance and the multiplier checks).
+int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
+    if (n < 2 || !lu_nopiv_enabled()) return 1;
+    Scratch flags;
+    if (int rc = flags.alloc(16, s)) return rc;
+    int *d_flag = flags.as<int>();
+    unsigned long long *d_max = reinterpret_cast<unsigned long long *>(flags.as<char>() + 8);
+    LM_CUDA(cudaMemsetAsync(flags.p, 0, 16, s));
+    coldom_check<<<(unsigned)(4 * num_sms()), 256, 0, s>>>(A, n, lda, d_flag);
+    LM_LAUNCHED(1);
+    int h_flag = 1;
+    LM_CUDA(cudaMemcpyAsync(&h_flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LM_CUDA(cudaStreamSynchronize(s));
+    if (h_flag) return 1;
+    Scratch backup;  // the original matrix, in case the multiplier check fails
+    if (int rc = backup.alloc(sizeof(double) * (size_t)n * n, s)) return rc;
+    LM_CUDA(cudaMemcpy2DAsync(backup.p, n * sizeof(double), A, lda * sizeof(double), n * sizeof(double), n,
+                              cudaMemcpyDeviceToDevice, s));
+    if (int rc = nopiv_factor(A, n, lda, s)) return rc;
+    lower_absmax<<<(unsigned)(4 * num_sms()), 256, 0, s>>>(A, n, lda, d_max);
+    LM_LAUNCHED(1);
+    unsigned long long h_max = 0;
+    LM_CUDA(cudaMemcpyAsync(&h_max, d_max, sizeof(h_max), cudaMemcpyDeviceToHost, s));
+    LM_CUDA(cudaStreamSynchronize(s));
+    double mx;
+    memcpy(&mx, &h_max, sizeof(mx));
+    if (!(mx < kMulBound)) {  // not provably the reference's pivots: restore, let the caller pivot
+        LM_CUDA(cudaMemcpy2DAsync(A, lda * sizeof(double), backup.p, n * sizeof(double), n * sizeof(double), n,
+                                  cudaMemcpyDeviceToDevice, s));
+        return 1;
+    }
+    iota_piv<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(piv, n);
+    LM_LAUNCHED(1);
+    LM_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
+    return 0;
+}
+
+}  // namespace lm

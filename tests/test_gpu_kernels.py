@@ -384,6 +384,37 @@ def test_lu_factor_tensor_mode_pivots_and_residual(n):
     assert res <= 1e-10
 
 
+@pytest.mark.parametrize("kind", ["dominant", "general", "weakly_dominant"])
+def test_lu_tensor_mode_nopiv_path_2048(kind):
+    """n = 2048 in tensor mode: a column-dominant matrix takes the pivot-free
+    all-GEMM factorisation (pivoting provably never swaps: identity pivots,
+    what the reference computes); a general matrix, and one whose diagonal
+    is large but below the column sums (not provably swap-free), take the
+    pivoting path with the reference's pivots.  Residual <= 1e-10 either way."""
+    n = 2048
+    rng = np.random.default_rng(17)
+    a = rng.uniform(-1, 1, (n, n))
+    if kind == "dominant":
+        a[np.diag_indices(n)] += n
+    elif kind == "weakly_dominant":
+        a[np.diag_indices(n)] += 0.3 * n  # column sums of |a_ij| ~ n/2 > the diagonal: not provably swap-free
+    a = np.asfortranarray(a)
+    lu, piv = K.lu_factor(dev(a), mode="tensor")
+    ph = host(piv)
+    if kind == "dominant":
+        assert np.array_equal(ph, np.arange(n))
+    else:
+        rc, lu_ref, piv_ref = O.lu_factor(a)
+        assert np.array_equal(ph, piv_ref)
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, 3)))
+    x = dev(np.array(b, order="F"))
+    K.lu_solve_into(dev(a), x, mode="tensor")
+    xh = host(x)
+    res = np.linalg.norm(a @ xh - b, np.inf) / (np.linalg.norm(a, np.inf) * np.linalg.norm(xh, np.inf) +
+                                                np.linalg.norm(b, np.inf))
+    assert res <= 1e-10
+
+
 @pytest.mark.parametrize("n", [700, 1500])
 def test_lu_factor_large_general_bitwise(n):
     """Multi-CTA cluster panels, outer blocks and laswp: still the

@@ -1,1 +1,1 @@
-timeout 300 python tools/host_overhead_probe.py 2>&1 | head -60
+timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_fullsize.py -q -x -k "lu or config4a" 2>&1 | tail -2
