@@ -71,8 +71,9 @@ __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb
     __shared__ double a[NBD * LDD];  // (i, j) at a[j * LDD + i]
     const int tid = threadIdx.x;
     const int tx = tid & (NBD - 1), ty = tid >> 6;
-    for (int c = ty; c < nb; c += 8)
-        if (tx < nb) a[c * LDD + tx] = A[tx + (int64_t)c * lda];
+#pragma unroll
+    for (int c = ty; c < NBD; c += 8)
+        if (tx < nb && c < nb) a[c * LDD + tx] = A[tx + (int64_t)c * lda];
     __syncthreads();
     for (int k = 0; k < nb; ++k) {
         const double p = a[k * LDD + k];
@@ -88,60 +89,69 @@ __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb
         if (tx < nb) A[tx + (int64_t)c * lda] = a[c * LDD + tx];
 }
 
-// L21 = A21 U11^-1 in place: one thread per row of A21 (rows [0, M) at
-// A21, leading dimension lda), the row in registers (static indices: the
-// substitution is unrolled over the block width), U11 (nb x nb at U) in
-// shared memory.  Row-wise forward substitution x U = a:
-//   for i: x_i = s_i / u_ii; s_j -= x_i u_ij (j > i)
-__global__ void __launch_bounds__(128) trsm_right_upper(double *A21, int64_t lda, int64_t M, const double *U,
-                                                       int nb) {
-    __shared__ double u[NBD * LDD];  // (i, j) at u[j * LDD + i]
-    for (int e = threadIdx.x; e < NBD * NBD; e += blockDim.x) {
+// The two triangular solves keep a thread's row (or column) SHIFTED in
+// registers -- before step i, s[j] holds entry i + j -- so the step loop is
+// rolled with static register indices (the fully unrolled 64 x 64 solve is
+// ~8k instructions that every warp runs once: ncu showed 34% of the stalls
+// waiting on instruction fetch).  The triangle sits in shared memory padded
+// to 2 x 64 zero columns so entry i + j never leaves it.
+constexpr int kTriSmem = 2 * NBD * LDD * (int)sizeof(double);
+
+// L21 = A21 U11^-1 in place: one thread per row of A21 (rows [0, M),
+// leading dimension lda), U11 (nb x nb at U).  Row-wise substitution
+// x U = a:  x_i = s_i / u_ii;  s_j -= x_i u_ij (j > i)
+__global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda, int64_t M, const double *U, int nb) {
+    extern __shared__ double tsm[];  // u_ij at tsm[j * LDD + i], j < 2 * NBD (zero past nb)
+#pragma unroll 16
+    for (int e = threadIdx.x; e < 2 * NBD * NBD; e += blockDim.x) {
         const int i = e & (NBD - 1), j = e >> 6;
-        u[j * LDD + i] = (i < nb && j < nb) ? U[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+        tsm[j * LDD + i] = (i < nb && j < nb) ? U[i + (int64_t)j * lda] : (i == j && j < NBD ? 1.0 : 0.0);
     }
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= M) return;
-    double s[NBD];
+    double *row = A21 + r;
+    double sv[NBD];
 #pragma unroll
-    for (int c = 0; c < NBD; ++c) s[c] = c < nb ? A21[r + c * lda] : 0.0;
+    for (int c = 0; c < NBD; ++c) sv[c] = c < nb ? row[c * lda] : 0.0;
+#pragma unroll 1
+    for (int i = 0; i < nb; ++i) {
+        const double *ui = tsm + i;  // u_{i, i + j} at ui[(i + j) * LDD]
+        const double x = sv[0] / ui[i * LDD];
+        row[i * lda] = x;
 #pragma unroll
-    for (int i = 0; i < NBD; ++i) {
-        const double x = s[i] / u[i * LDD + i];
-        s[i] = x;
-#pragma unroll
-        for (int j = i + 1; j < NBD; ++j) s[j] = fma(-x, u[j * LDD + i], s[j]);
+        for (int j = 1; j < NBD; ++j) sv[j - 1] = fma(-x, ui[(i + j) * LDD], sv[j]);
+        sv[NBD - 1] = 0.0;
     }
-#pragma unroll
-    for (int c = 0; c < NBD; ++c)
-        if (c < nb) A21[r + c * lda] = s[c];
 }
 
 // U12 = L11^-1 A12 in place: one thread per column of A12 (nb rows, columns
-// [0, N) at A12), unit lower L11 (at L) in shared memory.
-//   for k: y_k final; y_i -= l_ik y_k (i > k)
-__global__ void __launch_bounds__(128) trsm_left_lower_unit(double *A12, int64_t lda, int64_t N, const double *L,
-                                                           int nb) {
-    __shared__ double l[NBD * LDD];  // (i, k) at l[k * LDD + i]
-    for (int e = threadIdx.x; e < NBD * NBD; e += blockDim.x) {
-        const int i = e & (NBD - 1), k = e >> 6;
-        l[k * LDD + i] = (i < nb && k < nb && i > k) ? L[i + (int64_t)k * lda] : 0.0;
+// [0, N)), unit lower L11 (at L).  y_k final; y_i -= l_ik y_k (i > k)
+__global__ void __launch_bounds__(64) trsm_left_lower_unit(double *A12, int64_t lda, int64_t N, const double *L,
+                                                          int nb) {
+    extern __shared__ double tsm[];  // l_ik at tsm[k * LDD2 + i], i < 2 * NBD (zero past nb / on and above the diagonal)
+    constexpr int LDD2 = 2 * NBD + 1;
+#pragma unroll 16
+    for (int e = threadIdx.x; e < NBD * 2 * NBD; e += blockDim.x) {
+        const int i = e % (2 * NBD), k = e / (2 * NBD);
+        tsm[k * LDD2 + i] = (i < nb && k < nb && i > k) ? L[i + (int64_t)k * lda] : 0.0;
     }
     __syncthreads();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= N) return;
-    double y[NBD];
     double *col = A12 + c * lda;
+    double y[NBD];
 #pragma unroll
     for (int i = 0; i < NBD; ++i) y[i] = i < nb ? col[i] : 0.0;
+#pragma unroll 1
+    for (int k = 0; k < nb; ++k) {
+        const double yk = y[0];
+        col[k] = yk;
+        const double *lk = tsm + k * LDD2 + k;  // l_{k + j, k} at lk[j]
 #pragma unroll
-    for (int k = 0; k < NBD; ++k)
-#pragma unroll
-        for (int i = k + 1; i < NBD; ++i) y[i] = fma(-l[k * LDD + i], y[k], y[i]);
-#pragma unroll
-    for (int i = 0; i < NBD; ++i)
-        if (i < nb) col[i] = y[i];
+        for (int j = 1; j < NBD; ++j) y[j - 1] = fma(-lk[j], yk, y[j]);
+        y[NBD - 1] = 0.0;
+    }
 }
 
 // max |l_ij| over the strictly lower triangle of the n x n factor (bit pattern
@@ -186,6 +196,8 @@ int nopiv_streams(NoPivStreams &st) {
 int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     NoPivStreams st;
     if (int rc = nopiv_streams(st)) return rc;
+    if (int rc = func_attrs(trsm_right_upper, kTriSmem)) return rc;
+    if (int rc = func_attrs(trsm_left_lower_unit, kTriSmem + 8 * NBD)) return rc;
     cudaEvent_t ev_fork, ev_l21, ev_rest, ev_join;
     LM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     LM_CUDA(cudaEventCreateWithFlags(&ev_l21, cudaEventDisableTiming));
@@ -207,7 +219,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     // LM_NOPIV_TRACE=1: per-phase device time on each stream (stderr)
     static const bool trace = getenv("LM_NOPIV_TRACE") != nullptr;
     std::vector<cudaEvent_t> evs;
-    std::vector<int> tags;  // 0 diag, 1 L21, 2 next panel, 3 rest (lo)
+    std::vector<int> tags;  // hi: 0 diag, 1 trsm_ru, 2 trsm_ll, 3 gemm, 4 wait for lo; 5 lo
     auto mark = [&](cudaStream_t str, int tag) {
         if (!trace) return;
         cudaEvent_t e;
@@ -225,13 +237,13 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     constexpr int OB = 2 * NBD;
     auto trsm_ru = [&](double *A21, int64_t M, const double *U, int nb, cudaStream_t str) -> int {
         if (M <= 0) return 0;
-        trsm_right_upper<<<(unsigned)ceil_div(M, 64), 64, 0, str>>>(A21, lda, M, U, nb);
+        trsm_right_upper<<<(unsigned)ceil_div(M, 64), 64, kTriSmem, str>>>(A21, lda, M, U, nb);
         LM_LAUNCHED(1);
         return 0;
     };
     auto trsm_ll = [&](double *A12, int64_t N, const double *L, int nb, cudaStream_t str) -> int {
         if (N <= 0) return 0;
-        trsm_left_lower_unit<<<(unsigned)ceil_div(N, 64), 64, 0, str>>>(A12, lda, N, L, nb);
+        trsm_left_lower_unit<<<(unsigned)ceil_div(N, 64), 64, kTriSmem + 8 * NBD, str>>>(A12, lda, N, L, nb);
         LM_LAUNCHED(1);
         return 0;
     };
@@ -248,43 +260,53 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         LM_LAUNCHED(1);
         mark(st.hi, 0);
         if (int rc = trsm_ru(A + Ja + J0 * lda, n - Ja, Aaa, na, st.hi)) return rc;  // L of block a, rows below a
+        mark(st.hi, 1);
         if (nbb > 0) {
             if (int rc = trsm_ll(A + J0 + Ja * lda, nbb, Aaa, na, st.hi)) return rc;  // U_ab
+            mark(st.hi, 2);
             if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + Ja * lda, lda, Abb, lda, n - Ja, nbb, na, st.hi))
                 return rc;
+            mark(st.hi, 3);
             diag_nopiv<<<1, 512, 0, st.hi>>>(Abb, lda, nbb);
             LM_LAUNCHED(1);
+            mark(st.hi, 0);
             if (int rc = trsm_ru(A + J1 + Ja * lda, n - J1, Abb, nbb, st.hi)) return rc;  // L of block b
+            mark(st.hi, 1);
         }
         LM_CUDA(cudaEventRecord(ev_l21, st.hi));
-        mark(st.hi, 1);
         if (J1 >= n) break;
         // ---- U12 of the outer block's rows over the columns [c0, c0 + nc), then
         // the rank-nob update of the rows below
-        auto u12 = [&](int64_t c0, int64_t nc, cudaStream_t str) -> int {
+        auto u12 = [&](int64_t c0, int64_t nc, cudaStream_t str, bool hi) -> int {
             if (int rc = trsm_ll(A + J0 + c0 * lda, nc, Aaa, na, str)) return rc;
+            if (hi) mark(str, 2);
             if (nbb > 0) {
                 if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + c0 * lda, lda, A + Ja + c0 * lda, lda, nbb, nc,
                                        na, str))
                     return rc;
+                if (hi) mark(str, 3);
                 if (int rc = trsm_ll(A + Ja + c0 * lda, nc, Abb, nbb, str)) return rc;
+                if (hi) mark(str, 2);
             }
-            return dgemm_sub(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1, nc, nob,
-                             str);
+            if (int rc = dgemm_sub(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1, nc,
+                                   nob, str))
+                return rc;
+            if (hi) mark(str, 3);
+            return 0;
         };
         // the remaining columns on the low-priority stream (after the previous
         // outer block's, which wrote the same columns)
         const int64_t nn2 = n - J2;
         if (nn2 > 0) {
             LM_CUDA(cudaStreamWaitEvent(st.lo, ev_l21, 0));
-            if (int rc = u12(J2, nn2, st.lo)) return rc;
-            mark(st.lo, 3);
+            if (int rc = u12(J2, nn2, st.lo, false)) return rc;
+            mark(st.lo, 5);
         }
         // the next outer panel's columns were last written by the previous
         // block's trailing update: wait for it, then their U12 and update
         if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
-        if (int rc = u12(J1, J2 - J1, st.hi)) return rc;
-        mark(st.hi, 2);
+        mark(st.hi, 4);
+        if (int rc = u12(J1, J2 - J1, st.hi, true)) return rc;
         rest_pending = nn2 > 0;
         if (rest_pending) LM_CUDA(cudaEventRecord(ev_rest, st.lo));
     }
@@ -292,18 +314,18 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         const double host_us =
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
         cudaDeviceSynchronize();
-        double tot[4] = {0, 0, 0, 0}, last_hi = 0, last_lo = 0;
+        double tot[6] = {0, 0, 0, 0, 0, 0}, last_hi = 0, last_lo = 0;
         float t;
         for (size_t i = 2; i < evs.size(); ++i) {
-            const bool lo = tags[i] == 3;
+            const bool lo = tags[i] == 5;
             cudaEventElapsedTime(&t, evs[0], evs[i]);
             double &last = lo ? last_lo : last_hi;
             tot[tags[i]] += t - last;
             last = t;
         }
-        fprintf(stderr, "NOPIVTRACE host issue %.0f us | hi: diag %.2f ms, L21 %.2f ms, next panel (incl. wait) %.2f ms, "
-                        "end %.2f ms | lo: rest end %.2f ms (busy %.2f)\n",
-                host_us, tot[0], tot[1], tot[2], last_hi, last_lo, tot[3]);
+        fprintf(stderr, "NOPIVTRACE host issue %.0f us | hi: diag %.2f ms, trsm_ru %.2f, trsm_ll %.2f, gemm %.2f, "
+                        "wait for lo %.2f, end %.2f ms | lo: end %.2f ms\n",
+                host_us, tot[0], tot[1], tot[2], tot[3], tot[4], last_hi, last_lo);
         for (auto e : evs) cudaEventDestroy(e);
     }
     if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
