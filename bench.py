@@ -947,7 +947,10 @@ class Config5a(Workload):
         import torch
         from paper_2502_03000_b200.batch import atb_schur_trace, empty_batch
         tdt, w = self._tdt(), self.width
-        k = {n: min(self.e2e_per_class, c) for n, c in self.rank_counts().items()}
+        # a rate: the per-rank sample shrinks with the world size so N ranks pin
+        # about as much host memory as one
+        per = max(1024, self.e2e_per_class // max(self.ws, 1))
+        k = {n: min(per, c) for n, c in self.rank_counts().items()}
         host_in, dev_in, host_out, dev_out = {}, {}, {}, {}
         for n in self.SIZES:
             if not k[n]:
@@ -982,7 +985,7 @@ class Config5a(Workload):
             torch.cuda.synchronize()
             return [v for n in host_out for v in host_out[n]]
         self.e2e_work = self._bytes(k)
-        self.e2e_sample = f"{self.e2e_per_class} instances of each size class per rank, chunks of {CH}"
+        self.e2e_sample = f"{per} instances of each size class per rank, chunks of {CH}"
         return run, sum(4 * c * n * n * w for n, c in k.items()), sum(c * (n * n + 1) * w for n, c in k.items())
 
 
