@@ -498,7 +498,8 @@ def test_chain_plan_fused_with_identical_events(monkeypatch):
     """X*Y*Z through evaluate() with the chain fusion on (LM_GEMM_CHAIN=1):
     the executor fuses the two gemm steps into one launch but records exactly
     the events of the two-step plan."""
-    from paper_2502_03000_b200 import rewrite as rw
+    import importlib
+    rw = importlib.import_module("paper_2502_03000_b200.rewrite")  # the module (the package exports a function of that name)
     monkeypatch.setattr(rw, "_CHAIN_ON", True)
     rng = np.random.default_rng(3)
     X, Y, Z = (lm.DenseMatrix(np.asfortranarray(rng.uniform(-1, 1, s))) for s in ((500, 40), (40, 700), (700, 40)))
