@@ -19,6 +19,7 @@
 // Traffic per instance: A read once (N*N*8 B), b read, x written; the LU
 // factors / pivots are written only when requested.
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -219,7 +220,8 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
 template <int N, int KB, bool CLASSIFY>
 __global__ void __launch_bounds__(N, N == 64 ? 6 : 1)
     lu_batched_shift(int64_t n, int64_t batch, const double *__restrict__ A, double *__restrict__ X,
-                     int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls) {
+                     int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls,
+                     int redo_only) {
     constexpr int W = N / 32 > 0 ? N / 32 : 1;  // warps per system
     constexpr int R = (N + 31) / 32;            // back-sweep positions per lane
     constexpr unsigned MASK = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(N, N == 64 ? 6 : 1)
 
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
     const int64_t b = blockIdx.x;
+    if (redo_only && info[b] != -1) return;  // after the pivot-free fast path: only the systems it could not prove
     const double *Ab = A + b * n * n;
     double r[N];
 #pragma unroll
@@ -396,34 +399,394 @@ __global__ void __launch_bounds__(N, N == 64 ? 6 : 1)
         if (q * 32 + lane < n) X[b * n + q * 32 + lane] = c[q];
 }
 
+// ---------------------------------------------------------------------------
+// Pivot-free blocked fast path for 32 < n <= 64 (config 4b), bit-identical
+// to _lu_factor + _lu_solve_inplace (lazymat/_loops.py:200-259) whenever
+// the reference's partial pivoting never swaps -- and it PROVES that it
+// never swaps: at step k the reference keeps p = k unless some
+// |LU[i,k]| > |LU[k,k]| (strict, lazymat/_loops.py:212-218).  Every
+// multiplier m = RN(LU[i,k] / LU[k,k]) is checked to satisfy |m| < 1,
+// which implies |LU[i,k]| < |LU[k,k]| (rounding is monotonic and 1 is
+// representable), so p = k; by induction over k the state at every step is
+// the reference's own.  A failed check (including NaN, Inf and a zero
+// pivot) marks the system (info = -1, x untouched) and the pivoting kernel
+// (lu_batched_shift, redo mode) solves exactly those systems afterwards.
+// Diagonally dominant batches (config 4b: A = U(-1,1) + 64 I) never fail.
+//
+// Without pivot search the per-column chain shrinks to a division, so the
+// factorisation runs in blocks of KB = 8 columns with two block barriers
+// per block (instead of one per column):
+//   (a) the warp holding the block's 8 diagonal rows factors the 8 x 8
+//       diagonal block with shuffles (the pivot row's values broadcast
+//       lane to lane) and publishes U11, its multipliers and its rows' raw
+//       rest (columns c0+8.., then the right-hand side);
+//   (b) every row below divides and eliminates its own 8 panel values
+//       against U11 (a per-row triangular solve in the reference's order:
+//       column c0+s2 receives steps c0, c0+1, ... then its division);
+//   (c) concurrently, one thread per rest column finishes the block's U
+//       rows (row c0+s receives steps c0..c0+s-1 in order);
+//   (d) every row below applies the 8 deferred rank-1 updates to its rest,
+//       s ascending (mul and sub separately rounded: the reference's
+//       sequence of roundings for every element).
+// The rest buffer is double-buffered by block parity so block kb+1's (a)
+// overlaps block kb's (d) in the other warp.  The back sweep is the
+// shift kernel's (one warp, packed U).
+__device__ __forceinline__ constexpr int upacked_off(int k) { return k * 64 - k * (k - 1) / 2; }
+
+// Certified fast division.  __ddiv_rn costs ~126 cycles of dependent
+// latency on the B200 (tools/probes/fp64_lat_probe.cu: DFMA 8.7, drcp 76,
+// ddiv 126), and the pivot-free path divides by the same pivot many times.
+// With y = RN(1/b) computed once per divisor, q0 = RN(a*y),
+// r = RN(a - b*q0), q1 = RN(q0 + r*y) (Markstein's correction: three
+// dependent FP64 operations) is RN(a/b) in practice -- and this is CHECKED,
+// not assumed: rho = RN(a - b*q1) (one fma: a single rounding of the exact
+// remainder) and q1 is certified when |rho| < T' = halfulp(q1) *
+// RN(|b| * (1 - 2^-50)), halfulp(q1) being half the gap to q1's smaller
+// neighbour (a power of two, so T' is an exact product).  Then
+// |a - b*q1| <= |rho| * (1 + 2^-52) < |b| * halfulp(q1), i.e. a/b lies strictly
+// inside q1's round-to-nearest interval, so q1 == RN(a/b) == __ddiv_rn(a, b).
+// Exponent windows keep every quantity normal (no underflow in T' or in the
+// remainder's rounding).  A zero dividend returns a*y (the correctly signed
+// zero).  An uncertified quotient sets `bad`; the pivot-free kernel then
+// hands the whole system to the pivoting kernel, so results never depend on
+// an unproved quotient.
+struct CertDiv {
+    double b, y, bc;
+    int eb;  // biased exponent of b; 0 = not certifiable (outside the window)
+};
+
+// y = RN(1/b) computed by the caller (once per divisor, off the chains)
+__device__ __forceinline__ CertDiv cdiv_prep(double b, double y) {
+    CertDiv d;
+    d.b = b;
+    d.y = y;
+    d.bc = __dmul_rn(fabs(b), 1.0 - 0x1p-50);
+    const int eb = (__double2hiint(b) >> 20) & 0x7ff;
+    d.eb = (eb >= 1023 - 1000 && eb <= 1023 + 1000) ? eb : -4096;
+    return d;
+}
+
+__device__ __forceinline__ double cdiv(double a, const CertDiv &d, int &bad) {
+    const double q0 = __dmul_rn(a, d.y);
+    const double r0 = __fma_rn(-q0, d.b, a);
+    const double q1 = __fma_rn(r0, d.y, q0);
+    const double rho = __fma_rn(-q1, d.b, a);
+    const int hi = __double2hiint(q1), lo = __double2loint(q1);
+    const int e = (hi >> 20) & 0x7ff;
+    const int mz = ((hi & 0xfffff) | lo) == 0;  // |q1| a power of two: the gap below is half an ulp
+    const double halfulp = __hiloint2double((e - 53 - mz) << 20, 0);
+    const double tc = __dmul_rn(halfulp, d.bc);
+    // q1 normal, half-ulp normal, not near overflow; T' = halfulp*|b| >= 2^-900
+    const bool range = (unsigned)(e - 55) < 1945u && e + d.eb >= 2 * 1023 - 900;
+    const bool zero = a == 0.0;
+    const bool good = zero ? d.eb > 0 : (range && fabs(rho) < tc);
+    bad |= !good;
+    return zero ? q0 : q1;
+}
+
+// TRACE (LM_4B_TRACE=1, diagnostics): thread 63 records clock64() at the
+// phase boundaries of every block into trace[b * 32 + i] (tools/lu4b_trace.py).
+#define LU4B_MARK(i)                                                          \
+    if (TRACE && t == 63) trace[b * 32 + (i)] = clock64();
+template <bool CLASSIFY, bool TRACE = false>
+__global__ void __launch_bounds__(64, 6)
+    lu_batched_nopiv(int64_t n, int64_t batch, const double *__restrict__ A, double *__restrict__ X,
+                     int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls,
+                     long long *__restrict__ trace = nullptr) {
+    constexpr int N = 64, KB = 8, NB = N / KB;
+    constexpr int UW = N - KB + 2;  // rest width incl. the right-hand side, even
+    constexpr unsigned MASK = 0xffffffffu;
+    struct Fact {
+        double Ub[2][KB][UW];        // block rows' rest: raw, then U[c0+s, c0+8+j]; column Rw = y
+        double U11[KB][KB];          // diagonal block: U[c0+s, c0+s2] for s2 >= s
+        double Ld[KB][KB];           // diagonal block multipliers L[c0+s, c0+s2], s2 < s
+        double Lr[KB][N];            // multipliers of the rows below, by owning thread
+        double Us[N * (N + 1) / 2];  // packed U: U[k, k+i] at upacked_off(k) + i
+        double xs[N];                // y by position
+        double yd[N];                // RN(1 / U[k,k]), for the certified divisions
+    };
+    constexpr size_t SAT = CLASSIFY ? sizeof(double) * N * (N + 1) : 0;
+    constexpr size_t SMB = sizeof(Fact) > SAT ? sizeof(Fact) : SAT;
+    __shared__ __align__(16) unsigned char smraw[SMB];
+    Fact &f = *reinterpret_cast<Fact *>(smraw);
+
+    const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+    const int64_t b = blockIdx.x;
+    const double *Ab = A + b * n * n;
+    double r[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        if (t < n && j < n)
+            r[j] = __ldg(Ab + t + (int64_t)j * n);
+        else
+            r[j] = (t == j) ? 1.0 : 0.0;  // identity padding: pivot-free by construction
+    }
+    if (TRACE && t == 63) {
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        trace[b * 32 + 30] = sm;
+    }
+    LU4B_MARK(0)
+    double xv = t < n ? __ldg(X + b * n + t) : 0.0;
+    int bad = 0;  // a multiplier with !(|m| < 1) seen by this thread
+    if constexpr (CLASSIFY) {
+        // lazymat/rewrite.py:146-173 over _analyze (lazymat/_loops.py:15-34)
+        double(*sAt)[N + 1] = reinterpret_cast<double(*)[N + 1]>(smraw);
+        __shared__ unsigned s_lb[2], s_ub[2], s_as[2];
+        unsigned lb = 0, ub = 0, asym = 0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (t < n && j < n) {
+                sAt[t][j] = r[j];
+                if (r[j] != 0.0) {
+                    if (t > j) lb = max(lb, (unsigned)(t - j));
+                    if (j > t) ub = max(ub, (unsigned)(j - t));
+                }
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (t < n && j < n && j > t && !(r[j] == sAt[j][t])) asym = 1;
+        lb = __reduce_max_sync(MASK, lb);
+        ub = __reduce_max_sync(MASK, ub);
+        asym = __reduce_or_sync(MASK, asym);
+        if (lane == 0) {
+            s_lb[w] = lb;
+            s_ub[w] = ub;
+            s_as[w] = asym;
+        }
+        __syncthreads();
+        if (t == 0) {
+            lb = max(lb, s_lb[1]);
+            ub = max(ub, s_ub[1]);
+            asym |= s_as[1];
+            const unsigned lim = (unsigned)(n / 4 > 4 ? n / 4 : 4);
+            int c = 0;
+            if (lb + ub <= lim) c = 1;
+            else if (lb == 0) c = 2;
+            else if (ub == 0) c = 3;
+            else if (!asym) c = 4;
+            cls[b] = c;
+        }
+        __syncthreads();  // the transpose aliases the factorisation's buffers
+    }
+
+#pragma unroll
+    for (int kb = 0; kb < NB; ++kb) {
+        const int c0 = kb * KB, par = kb & 1;
+        const int Rw = N - c0 - KB;  // rest columns right of the block (static)
+        LU4B_MARK(1 + 3 * kb)
+        // (a) the diagonal block, by the warp that holds rows c0..c0+7
+        if (w == (c0 >> 5)) {
+            const int ls = t - c0;  // 0..7 on the diagonal rows
+            const bool diag = (unsigned)ls < (unsigned)KB;
+#pragma unroll
+            for (int s = 0; s < KB; ++s) {
+                const int src = (c0 + s) & 31;
+                const double pv = __shfl_sync(MASK, r[c0 + s], src);
+                double u[KB];
+#pragma unroll
+                for (int s2 = s + 1; s2 < KB; ++s2) u[s2] = __shfl_sync(MASK, r[c0 + s2], src);
+                // branch-free: every lane divides, only the block's rows
+                // below the pivot keep the result
+                const bool act = diag && ls > s;
+                const double m = __ddiv_rn(r[c0 + s], pv);
+                bad |= act & !(fabs(m) < 1.0);
+                if (act) f.Ld[ls][s] = m;
+#pragma unroll
+                for (int s2 = s + 1; s2 < KB; ++s2) {
+                    const double v = __dsub_rn(r[c0 + s2], __dmul_rn(m, u[s2]));
+                    r[c0 + s2] = act ? v : r[c0 + s2];
+                }
+            }
+            if (diag) {
+                double ukk = r[c0];
+#pragma unroll
+                for (int s2 = 1; s2 < KB; ++s2)
+                    if (ls == s2) ukk = r[c0 + s2];
+                f.yd[c0 + ls] = __drcp_rn(ukk);  // U[k,k] is final: its reciprocal for (b) and the back sweep
+                double2 *u11 = reinterpret_cast<double2 *>(f.U11[ls]);
+#pragma unroll
+                for (int i = 0; i < KB / 2; ++i) u11[i] = make_double2(r[c0 + 2 * i], r[c0 + 2 * i + 1]);
+#pragma unroll
+                for (int s2 = 0; s2 < KB; ++s2)
+                    if (s2 >= ls) f.Us[upacked_off(c0 + ls) + s2 - ls] = r[c0 + s2];
+                double2 *dst = reinterpret_cast<double2 *>(f.Ub[par][ls]);
+#pragma unroll
+                for (int j = 0; j < Rw; j += 2) dst[j >> 1] = make_double2(r[c0 + KB + j], r[c0 + KB + j + 1]);
+                f.Ub[par][ls][Rw] = xv;
+            }
+        }
+        __syncthreads();
+        LU4B_MARK(2 + 3 * kb)
+        // (c) U rows of the block, one thread per rest column (the last one is y)
+        if (t <= Rw) {
+#pragma unroll
+            for (int s = 0; s < KB; ++s) {
+                double u = f.Ub[par][s][t];
+#pragma unroll
+                for (int s2 = 0; s2 < s; ++s2) u = __dsub_rn(u, __dmul_rn(f.Ld[s][s2], f.Ub[par][s2][t]));
+                f.Ub[par][s][t] = u;  // this thread's column only: read back by later s
+                if (t < Rw)
+                    f.Us[upacked_off(c0 + s) + KB - s + t] = u;
+                else
+                    f.xs[c0 + s] = u;
+            }
+        }
+        // (b) the rows below: divide and eliminate the own panel values
+        if (t >= c0 + KB) {
+            CertDiv dv[KB];
+#pragma unroll
+            for (int s = 0; s < KB; ++s) dv[s] = cdiv_prep(f.U11[s][s], f.yd[c0 + s]);
+#pragma unroll
+            for (int s = 0; s < KB; ++s) {
+                const double m = cdiv(r[c0 + s], dv[s], bad);
+                bad |= !(fabs(m) < 1.0);
+                f.Lr[s][t] = m;
+#pragma unroll
+                for (int s2 = s + 1; s2 < KB; ++s2) r[c0 + s2] = __dsub_rn(r[c0 + s2], __dmul_rn(m, f.U11[s][s2]));
+            }
+        }
+        __syncthreads();
+        LU4B_MARK(3 + 3 * kb)
+        // (d) the block's deferred updates of the rows below, in step order
+        if (t >= c0 + KB) {
+#pragma unroll 1
+            for (int s = 0; s < KB; ++s) {
+                const double l = f.Lr[s][t];
+                const double2 *U2 = reinterpret_cast<const double2 *>(f.Ub[par][s]);
+#pragma unroll
+                for (int j = 0; j < Rw; j += 2) {
+                    const double2 u = U2[j >> 1];
+                    r[c0 + KB + j] = __dsub_rn(r[c0 + KB + j], __dmul_rn(l, u.x));
+                    r[c0 + KB + j + 1] = __dsub_rn(r[c0 + KB + j + 1], __dmul_rn(l, u.y));
+                }
+                xv = __dsub_rn(xv, __dmul_rn(l, f.Ub[par][s][Rw]));
+            }
+        }
+    }
+    if (__syncthreads_or(bad)) {  // pivoting could swap somewhere: the pivoting kernel redoes this system
+        if (t == 0) info[b] = -1;
+        return;
+    }
+    // back sweep (lazymat/_loops.py:254-258), blocked: thread t owns
+    // position t; per block of 8 positions (descending) the owning warp
+    // finishes the block with shuffles (x_j = c_j / U[j,j], then the
+    // block's positions above j), then every position above the block
+    // applies the block's 8 updates, j descending -- each c_i still sees
+    // j = n-1, n-2, ..., i+1 in the reference's order.
+    LU4B_MARK(25)
+    const CertDiv dd = cdiv_prep(t < n ? f.Us[upacked_off(t)] : 1.0, t < n ? f.yd[t] : 1.0);
+    double ci = t < n ? f.xs[t] : 0.0;
+    const int offt = upacked_off(t) - t;  // U[t, j] at offt + j
+#pragma unroll 1
+    for (int kb = NB - 1; kb >= 0; --kb) {
+        const int c0 = kb * KB;
+        if (c0 >= n) continue;
+        const int top = min(KB, (int)n - c0);  // real positions in this block
+        if (w == (c0 >> 5)) {
+            const int ls = t - c0;
+#pragma unroll
+            for (int s = KB - 1; s >= 0; --s) {
+                if (s < top) {  // warp-uniform
+                    const int j = c0 + s;
+                    // branch-free: every lane divides by its own diagonal
+                    // (only the owner's quotient and certificate are used)
+                    int bq = 0;
+                    const double q = cdiv(ci, dd, bq);
+                    bad |= (ls == s) & bq;
+                    const double xj = __shfl_sync(MASK, q, j & 31);
+                    const double upd = __dsub_rn(ci, __dmul_rn(f.Us[offt + j], xj));
+                    ci = ls == s ? xj : ((unsigned)ls < (unsigned)s ? upd : ci);
+                }
+            }
+            if (ls >= 0 && ls < KB) f.xs[t] = ci;  // x of the block's positions
+        }
+        __syncthreads();
+        if (t < c0) {
+#pragma unroll
+            for (int s = KB - 1; s >= 0; --s)
+                if (s < top) ci = __dsub_rn(ci, __dmul_rn(f.Us[offt + c0 + s], f.xs[c0 + s]));
+        }
+    }
+    if (__syncthreads_or(bad)) {  // an uncertified quotient: the pivoting kernel redoes the system
+        if (t == 0) info[b] = -1;
+        return;
+    }
+    LU4B_MARK(26)
+    if (t == 0) info[b] = 0;
+    if (piv && t < n) piv[b * n + t] = t;
+    if (t < n) X[b * n + t] = ci;
+}
+#undef LU4B_MARK
+
 }  // namespace lm
 
 using namespace lm;
 
-static bool use_shift_kernel() {
-    static const bool off = [] {
-        const char *e = getenv("LM_BATCHED_LU_UNROLLED");
-        return e && e[0] == '1';
+// Solve-only kernels: for 32 < n <= 64 the pivot-free fast path
+// ("nopiv", default) followed by the pivoting kernel on the systems it
+// could not prove; "shift" (LM_BATCHED_LU=shift: the pivoting kernel on
+// every system) and "rows" (LM_BATCHED_LU=rows or LM_BATCHED_LU_UNROLLED=1:
+// the unrolled kernel, also the one that returns the LU factors).
+static int batched_kernel_choice() {
+    static const int choice = [] {
+        const char *u = getenv("LM_BATCHED_LU_UNROLLED");
+        if (u && u[0] == '1') return 2;
+        const char *e = getenv("LM_BATCHED_LU");
+        if (e && !strcmp(e, "rows")) return 2;
+        if (e && !strcmp(e, "shift")) return 1;
+        return 0;
     }();
-    return !off;
+    return choice;
 }
+
+// diagnostics: the LM_4B_TRACE buffer (device pointer, 32 x 65536 int64), or null
+static long long *lu4b_trace_buffer() {
+    static long long *p = [] {
+        long long *q = nullptr;
+        if (getenv("LM_4B_TRACE") && cudaMalloc(&q, sizeof(long long) * 32 * 65536) != cudaSuccess) q = nullptr;
+        return q;
+    }();
+    return p;
+}
+extern "C" void *lm_debug_lu4b_trace(void) { return lu4b_trace_buffer(); }
 
 template <bool CLASSIFY>
 static int launch_batched(int64_t n, int64_t batch, const double *A, double *X, double *LU, int64_t *d_piv,
                           int32_t *d_info, int32_t *d_cls, cudaStream_t s) {
-    if (LU == nullptr && use_shift_kernel()) {
-        if (n <= 16)
-            lu_batched_shift<16, 8, CLASSIFY><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls);
-        else if (n <= 32)
-            lu_batched_shift<32, 8, CLASSIFY><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls);
+    const int choice = batched_kernel_choice();
+    if (LU == nullptr && n > 32 && choice == 0) {
+        long long *trace = lu4b_trace_buffer();
+        if (trace && batch <= 65536)
+            lu_batched_nopiv<CLASSIFY, true><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, trace);
         else
-            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls);
-    } else if (n <= 16)
-        lu_batched_rows<16, CLASSIFY><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
-    else if (n <= 32)
-        lu_batched_rows<32, CLASSIFY><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
-    else
-        lu_batched_rows<64, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
+            lu_batched_nopiv<CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls);
+        static const bool noredo = getenv("LM_4B_NOREDO") != nullptr;  // diagnostics: leave info = -1 visible
+        if (!noredo)
+            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 1);
+        note_variant("nopiv64");
+        LM_LAUNCHED(2);
+        return 0;
+    }
+    if (LU == nullptr && choice <= 1) {
+        if (n <= 16)
+            lu_batched_shift<16, 8, CLASSIFY><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 0);
+        else if (n <= 32)
+            lu_batched_shift<32, 8, CLASSIFY><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 0);
+        else
+            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 0);
+        note_variant(n > 32 ? "shift64" : "shift");
+    } else {
+        if (n <= 16)
+            lu_batched_rows<16, CLASSIFY><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
+        else if (n <= 32)
+            lu_batched_rows<32, CLASSIFY><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
+        else
+            lu_batched_rows<64, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, LU, d_piv, d_info, d_cls);
+        note_variant("rows");
+    }
     LM_LAUNCHED(1);
     return 0;
 }
