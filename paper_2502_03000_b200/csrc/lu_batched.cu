@@ -484,10 +484,10 @@ __device__ __forceinline__ double cdiv(double a, const CertDiv &d, int &bad) {
     return zero ? q0 : q1;
 }
 
-// TRACE (LM_4B_TRACE=1, diagnostics): thread 63 records clock64() at the
-// phase boundaries of every block into trace[b * 32 + i] (tools/lu4b_trace.py).
+// TRACE (LM_4B_TRACE=1, diagnostics): lane 0 of each warp records clock64()
+// at the phase boundaries into trace[b * 64 + warp * 32 + i] (tools/lu4b_trace.py).
 #define LU4B_MARK(i)                                                          \
-    if (TRACE && t == 63) trace[b * 32 + (i)] = clock64();
+    if (TRACE && lane == 0) trace[b * 64 + w * 32 + (i)] = clock64();
 template <bool CLASSIFY, bool TRACE = false>
 __global__ void __launch_bounds__(64, 6)
     lu_batched_nopiv(int64_t n, int64_t batch, const double *__restrict__ A, double *__restrict__ X,
@@ -521,10 +521,10 @@ __global__ void __launch_bounds__(64, 6)
         else
             r[j] = (t == j) ? 1.0 : 0.0;  // identity padding: pivot-free by construction
     }
-    if (TRACE && t == 63) {
+    if (TRACE && lane == 0) {
         unsigned sm;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-        trace[b * 32 + 30] = sm;
+        trace[b * 64 + w * 32 + 31] = sm;
     }
     LU4B_MARK(0)
     double xv = t < n ? __ldg(X + b * n + t) : 0.0;
@@ -634,6 +634,7 @@ __global__ void __launch_bounds__(64, 6)
                     f.xs[c0 + s] = u;
             }
         }
+        if (TRACE && lane == 0 && kb < 4) trace[b * 64 + w * 32 + 27 + kb] = clock64();  // (c) done
         // (b) the rows below: divide and eliminate the own panel values
         if (t >= c0 + KB) {
             CertDiv dv[KB];
@@ -742,11 +743,11 @@ static int batched_kernel_choice() {
     return choice;
 }
 
-// diagnostics: the LM_4B_TRACE buffer (device pointer, 32 x 65536 int64), or null
+// diagnostics: the LM_4B_TRACE buffer (device pointer, 64 x 65536 int64), or null
 static long long *lu4b_trace_buffer() {
     static long long *p = [] {
         long long *q = nullptr;
-        if (getenv("LM_4B_TRACE") && cudaMalloc(&q, sizeof(long long) * 32 * 65536) != cudaSuccess) q = nullptr;
+        if (getenv("LM_4B_TRACE") && cudaMalloc(&q, sizeof(long long) * 64 * 65536) != cudaSuccess) q = nullptr;
         return q;
     }();
     return p;
