@@ -219,3 +219,67 @@ def test_misaligned_operands_take_the_generic_kernel(which):
         assert np.max(np.abs(Eh[i] - Er)) <= 1e-12 * np.max(np.abs(Er))
         tr = O.trace_of_product(A, B)
         assert abs(sh[i] - tr) <= 1e-12 * max(abs(tr), 1.0)
+
+
+def _batched_lu_vs_oracle(A, b):
+    """lm_lu_solve_batched (solve only) vs the oracle's lu_factor + lu_solve:
+    x bitwise, info equal; returns the number of systems checked."""
+    from paper_2502_03000_b200 import _native as N
+
+    bt, n, _ = A.shape
+    x = torch.tensor(b[:, :, 0], device="cuda").contiguous()
+    piv = torch.zeros((bt, n), dtype=torch.int64, device="cuda")
+    info = torch.zeros(bt, dtype=torch.int32, device="cuda")
+    N.call("lm_lu_solve_batched", 0, n, bt, stack_fortran(A).data_ptr(), x.data_ptr(), None, piv.data_ptr(),
+           info.data_ptr())
+    torch.cuda.synchronize()
+    xs, ps, inf = x.cpu().numpy(), piv.cpu().numpy(), info.cpu().numpy()
+    for i in range(bt):
+        rc, lur, pr = O.lu_factor(np.asfortranarray(A[i]))
+        assert inf[i] == rc, (i, inf[i], rc)
+        if rc:
+            continue
+        assert np.array_equal(ps[i], pr), i
+        xr = np.array(b[i], order="F")
+        O.lu_solve(lur, pr, xr)
+        assert bits_equal(xs[i], xr[:, 0]), i
+    return bt
+
+
+@pytest.mark.parametrize("n", [33, 40, 57, 64])
+def test_lu_solve_batched_pivot_free_path_edges(n):
+    """The pivot-free fast path (n in 33..64) certifies every quotient and
+    proves identity pivots (|multiplier| < 1); whatever it cannot certify
+    falls to the pivoting kernel.  Edge systems: magnitudes scaled by 2^-600
+    / 2^600 (outside the certified exponent window), exact zeros in A and b,
+    power-of-two entries (quotients on binade boundaries), a multiplier of
+    exactly 1 (|a_ik| == |a_kk|: the reference keeps p = k, the fast path
+    must hand over), dominant and general matrices mixed in one batch.  x,
+    pivots and info bitwise vs the oracle."""
+    rng = np.random.default_rng(4000 + n)
+    bt = 24
+    A = rng.uniform(-1, 1, (bt, n, n)) + n * np.eye(n)[None]
+    b = rng.uniform(-1, 1, (bt, n, 1))
+    A[1] *= 2.0 ** -600
+    b[1] *= 2.0 ** -600
+    A[2] *= 2.0 ** 600
+    A[3][np.abs(A[3]) < 0.3] = 0.0
+    b[3][::3] = 0.0
+    A[4] = np.round(A[4] * 4) / 4 + n * np.eye(n)           # quarter-integers: many exact quotients
+    A[5] = 2.0 ** np.round(rng.uniform(-4, 4, (n, n)))      # powers of two, then dominant
+    A[5] += (2.0 * n * 16) * np.eye(n)
+    A[6][1, 0] = A[6][0, 0]                                 # |l_10| == 1 exactly
+    A[7] = rng.uniform(-1, 1, (n, n))                       # general: pivoting
+    A[8] = np.triu(A[8])
+    b[9] = 0.0
+    assert _batched_lu_vs_oracle(A, b) == bt
+
+
+def test_lu_solve_batched_default_is_pivot_free_kernel():
+    from paper_2502_03000_b200 import _native as N
+
+    rng = np.random.default_rng(5)
+    n, bt = 64, 3
+    A = rng.uniform(-1, 1, (bt, n, n)) + n * np.eye(n)[None]
+    _batched_lu_vs_oracle(A, rng.uniform(-1, 1, (bt, n, 1)))
+    assert N.last_variant() == "nopiv64"

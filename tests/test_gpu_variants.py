@@ -79,3 +79,42 @@ def test_f32_grouped_small_sizes_agree(n):
     assert ref["variant"] == f"tc_f32_{n}"
     assert got["variant"] == f"tc05p{n}"  # the grouped tcgen05 kernel really ran
     assert close(got["E"], ref["E"], 1e-5) and close(got["s"], ref["s"], 1e-5)
+
+
+LU_SCRIPT = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2502_03000_b200.batch import solve_batched, stack_fortran
+from paper_2502_03000_b200 import _native
+rng = np.random.default_rng(21)
+n, bt = 64, 300
+A = rng.uniform(-1, 1, (bt, n, n))
+A[::2] += n * np.eye(n)[None]          # dominant half: pivot-free path; the rest pivots
+b = rng.uniform(-1, 1, (bt, n, 1))
+x = solve_batched(stack_fortran(A), stack_fortran(b), check=False).x
+variant = _native.last_variant()
+print(json.dumps({"x": x.cpu().numpy().view(np.int64).ravel()[::7].tolist(), "variant": variant}))
+"""
+
+
+def run_lu(env_extra):
+    env = dict(os.environ)
+    env.update(env_extra)
+    out = subprocess.run([sys.executable, "-c", LU_SCRIPT, str(ROOT)], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("variant,kernel", [({"LM_BATCHED_LU": "shift"}, "shift64"),
+                                            ({"LM_BATCHED_LU": "rows"}, "rows")])
+def test_batched_lu_variants_bitwise(variant, kernel):
+    """Config 4b's kernels: the pivot-free fast path (default) against the
+    round-1 pivoting kernel on every system and the unrolled kernel, on a
+    batch where half the systems pivot: bit-identical solutions."""
+    ref = run_lu({})
+    assert ref["variant"] == "nopiv64"
+    got = run_lu(variant)
+    assert got["variant"] == kernel
+    assert got["x"] == ref["x"]
