@@ -25,6 +25,8 @@ arrays.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -100,6 +102,19 @@ def _classify(info, n):
     return band, triu, tril, symm
 
 
+_PINNED = threading.local()
+
+
+def _pinned_i32(count: int) -> torch.Tensor:
+    """A reusable pinned host buffer (per thread) for the (class, info)
+    read-back: a pageable .cpu() copy costs tens of microseconds more."""
+    buf = getattr(_PINNED, "i32", None)
+    if buf is None or buf.numel() < count:
+        buf = torch.empty(max(count, 1 << 14), dtype=torch.int32, pin_memory=True)
+        _PINNED.i32 = buf
+    return buf[:count]
+
+
 def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> BatchSolveResult:
     """inverse(A_i) * b_i for every instance (R9 -> R10 dispatch -> solve).
 
@@ -113,15 +128,21 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
     if n != n2 or b.shape[1] != n or b.shape[2] != 1:
         raise KernelContractError("solve_batched: A must be (batch, n, n) and b (batch, n, 1)")
     x = torch.empty((bt, 1, n), dtype=A.dtype, device=A.device).transpose(1, 2)
-    x.copy_(b)
+    if b.stride() == x.stride() and b.storage_offset() == 0 and b.untyped_storage().nbytes() == x.numel() * 8:
+        x.untyped_storage().copy_(b.untyped_storage(), non_blocking=True)  # one DMA copy, no kernel
+    else:
+        x.copy_(b)
     if n <= 64 and A.dtype == torch.float64:
         # one kernel: structure class + exact LU solve of every instance; one
-        # host read of (class, info)
+        # host read of (class, info) into pinned memory
         ci = torch.empty(2 * bt, dtype=torch.int32, device=A.device)
         N.call("lm_solve_batched_classified", N.dtype_code(A), n, bt, A.data_ptr(), x.data_ptr(), ci.data_ptr(),
                ci.data_ptr() + 4 * bt)
-        host = ci.cpu().numpy()
-        cls, hinfo = host[:bt].astype(np.int8), host[bt:]
+        host_t = _pinned_i32(2 * bt)
+        host_t.copy_(ci, non_blocking=True)
+        torch.cuda.current_stream(A.device).synchronize()
+        host = host_t.numpy()
+        cls, hinfo = host[:bt].astype(np.int8), host[bt:].copy()
     else:
         info = analyze_batched(A)
         band, triu, tril, symm = _classify(info, n)
