@@ -21,6 +21,9 @@
 // fixed, so results are reproducible.  FP64 FMA accumulation: results
 // match the reference's sequential sums to ~1e-15 normwise (north star:
 // <= 1e-12).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cmath>
 #include <cstdlib>
 
@@ -499,6 +502,250 @@ __global__ void __launch_bounds__(kGmThreads) dgemm_dmma(GemmArgs g) {
             }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant (the default where the operands allow it): every stage's
+// A and B tiles arrive by cp.async.bulk.tensor (one elected thread, per-
+// launch tensor maps, mbarrier completion by transaction bytes) in the
+// 128-byte swizzled layout, so a stage costs 2-5 TMA instructions instead of
+// 2 x 512 cp.async, and edge tiles need no predicated path (the tensor
+// engine zero-fills outside the tensor).  Tile layouts in shared memory:
+//   K-contiguous operand (KC): box {16 k, 64 outer}: row o = 128 B (k 0..15),
+//     16-byte chunk c at c ^ (o & 7);
+//   outer-contiguous operand (OC): 4 boxes {16 outer, 16 k}: box q = 2 KB,
+//     row k = 128 B (outer 16q..16q+15), chunk c at c ^ (k & 7).
+// Both make the m8n8k4 fragment loads hit the 2-wavefront minimum.  K
+// chunks of a split are multiples of 16, so a box never reads another
+// split's K range; only the tensor's own end is zero-filled.
+constexpr int kTmaTile = BM * BK * 8;  // bytes per operand tile (8 KB)
+
+template <bool KC> __device__ __forceinline__ double tfrag(const unsigned char *t, int o, int k) {
+    if (KC) return *reinterpret_cast<const double *>(t + o * 128 + ((((k >> 1) ^ (o & 7))) << 4) + ((k & 1) << 3));
+    return *reinterpret_cast<const double *>(t + ((o >> 4) << 11) + k * 128 + (((((o & 15) >> 1) ^ (k & 7))) << 4) +
+                                             ((o & 1) << 3));
+}
+
+__device__ __forceinline__ unsigned smaddr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void tma_wait(unsigned bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            bar),
+        "r"(parity)
+        : "memory");
+}
+
+template <bool KC>
+__device__ __forceinline__ void tma_tile(unsigned dst, const CUtensorMap *tm, int64_t o0, int64_t k0, unsigned bar) {
+    if (KC) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+                "r"(dst),
+            "l"(tm), "r"((int)k0), "r"((int)o0), "r"(bar)
+            : "memory");
+    } else {
+#pragma unroll
+        for (int q = 0; q < BM / 16; ++q)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+                "[%4];" ::"r"(dst + q * 2048),
+                "l"(tm), "r"((int)(o0 + 16 * q)), "r"((int)k0), "r"(bar)
+                : "memory");
+    }
+}
+
+// Warp-specialised: 4 MMA warps (2 x 2, warp tile 32 x 32) and one producer
+// warp; stages are handed over with full / empty mbarriers only -- no
+// CTA-wide barrier per K step (a __syncthreads every 64 DMMAs per warp lines
+// the warps up on the DMMA latency, tools/dmma_occ_probe.cu).
+constexpr int kGmTmaThreads = kGmThreads + 32;
+template <bool A_KC, bool B_KC, int ST>
+__global__ void __launch_bounds__(kGmTmaThreads) dgemm_dmma_tma(GemmArgs g, const __grid_constant__ CUtensorMap tmA,
+                                                               const __grid_constant__ CUtensorMap tmB) {
+    pdl_wait();  // inputs may be the previous kernel's output (PDL)
+    pdl_trigger();
+    extern __shared__ unsigned char tsm_raw[];
+    unsigned char *tsm = tsm_raw + ((1024 - (smaddr(tsm_raw) & 1023)) & 1023);  // 128B swizzle: 1 KB aligned
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(tsm + ST * 2 * kTmaTile);
+    unsigned long long *empty = full + ST;
+    int64_t tm, tn;
+    if (g.syrk) {
+        const int64_t idx = blockIdx.x;
+        int64_t t = (int64_t)((sqrt(8.0 * (double)idx + 1.0) - 1.0) * 0.5);
+        while ((t + 1) * (t + 2) / 2 <= idx) ++t;
+        while (t * (t + 1) / 2 > idx) --t;
+        tn = t;
+        tm = idx - t * (t + 1) / 2;
+    } else {
+        tm = blockIdx.x % ((g.M + BM - 1) / BM);
+        tn = blockIdx.x / ((g.M + BM - 1) / BM);
+    }
+    const int64_t m0 = tm * BM, n0 = tn * BN;
+    const int64_t kb = (int64_t)blockIdx.z * g.kchunk;
+    int64_t ke = kb + g.kchunk;
+    if (ke > g.K) ke = g.K;
+    const int64_t nk = ke > kb ? (ke - kb + BK - 1) / BK : 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < ST; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smaddr(&full[s])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smaddr(&empty[s])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 4) {  // producer
+        if (lane == 0) {
+            for (int64_t it = 0; it < nk; ++it) {
+                const int s = (int)(it % ST);
+                if (it >= ST) tma_wait(smaddr(&empty[s]), (unsigned)(((it / ST) - 1) & 1));
+                const unsigned bar = smaddr(&full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2u * kTmaTile)
+                             : "memory");
+                const int64_t k0 = kb + it * BK;
+                tma_tile<A_KC>(smaddr(tsm + s * 2 * kTmaTile), &tmA, m0, k0, bar);
+                tma_tile<B_KC>(smaddr(tsm + s * 2 * kTmaTile + kTmaTile), &tmB, n0, k0, bar);
+            }
+        }
+        return;
+    }
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int fr = lane >> 2, fc = lane & 3;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int64_t it = 0; it < nk; ++it) {
+        const int s = (int)(it % ST);
+        tma_wait(smaddr(&full[s]), (unsigned)((it / ST) & 1));
+        const unsigned char *a_s = tsm + s * 2 * kTmaTile;
+        const unsigned char *b_s = a_s + kTmaTile;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = tfrag<A_KC>(a_s, wm + i * 8 + fr, kk + fc);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = tfrag<B_KC>(b_s, wn + j * 8 + fr, kk + fc);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smaddr(&empty[s])) : "memory");
+    }
+    // epilogue (as dgemm_dmma)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t m = m0 + wm + i * 8 + fr, n = n0 + wn + j * 8 + 2 * fc + h;
+                if (m >= g.M || n >= g.N) continue;
+                const double v = acc[i][j][h];
+                if (g.part) {
+                    g.part[(int64_t)blockIdx.z * g.M * g.N + m + n * g.M] = v;
+                } else if (g.syrk) {
+                    if (tm == tn && m > n) continue;
+                    g.c[m * g.c_sm + n * g.c_sn] = v;
+                    g.c[n * g.c_sm + m * g.c_sn] = v;
+                } else if (g.sub) {
+                    double *pc = g.c + m * g.c_sm + n * g.c_sn;
+                    *pc = __dsub_rn(*pc, v);
+                } else {
+                    g.c[m * g.c_sm + n * g.c_sn] = v;
+                }
+            }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 gemm_tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+        PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return f;
+    }();
+    return enc;
+}
+
+// Tensor map of one operand: KC (K unit-stride): dims {K, outer}, box
+// {16, 64}; OC (outer unit-stride): dims {outer, K}, box {16, 16}; 128-byte
+// swizzle.  False when TMA cannot address it (alignment, strides, sizes).
+static bool gemm_tmap(CUtensorMap *tm, const double *base, bool kc, int64_t outer, int64_t K, int64_t stride) {
+    auto enc = gemm_tmap_encoder();
+    if (!enc || ((uintptr_t)base & 15) || (stride * 8) % 16 || stride <= 0 || outer > 0x7fffffff || K > 0x7fffffff ||
+        stride * 8 >= (1ll << 40))
+        return false;
+    cuuint64_t dims[2], strides[1] = {(cuuint64_t)(stride * 8)};
+    cuuint32_t box[2], es[2] = {1, 1};
+    if (kc) {
+        dims[0] = (cuuint64_t)K;
+        dims[1] = (cuuint64_t)outer;
+        box[0] = BK;
+        box[1] = BM;
+    } else {
+        dims[0] = (cuuint64_t)outer;
+        dims[1] = (cuuint64_t)K;
+        box[0] = 16;
+        box[1] = BK;
+    }
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool gemm_tma_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LM_GEMM_TMA");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <bool A_KC, bool B_KC, int ST>
+int launch_dgemm_tma_kernel(const GemmArgs &g, const CUtensorMap &ta, const CUtensorMap &tb, dim3 grid,
+                            cudaStream_t s) {
+    auto k = dgemm_dmma_tma<A_KC, B_KC, ST>;
+    constexpr int smem = ST * 2 * kTmaTile + 1024 + 16 * ST;
+    if (int rc = func_attrs(k, smem)) return rc;
+    LM_CUDA(launch_pdl(k, grid, dim3(kGmTmaThreads), smem, s, g, ta, tb));
+    LM_LAUNCHED(1);
+    note_variant("gemm_tma");
+    return 0;
+}
+
+// 0: launched; 1: not TMA-addressable (the caller launches the cp.async kernel)
+int try_launch_dgemm_tma(const GemmArgs &g, dim3 grid, cudaStream_t s) {
+    if (!gemm_tma_enabled() || g.sub) return 1;  // the LU's C -= A B keeps the tuned cp.async ring
+    const bool a_kc = g.a_sk == 1, b_kc = g.b_sk == 1;
+    if (!a_kc && g.a_sm != 1) return 1;
+    if (!b_kc && g.b_sn != 1) return 1;
+    CUtensorMap ta, tb;
+    if (!gemm_tmap(&ta, g.a, a_kc, g.M, g.K, a_kc ? g.a_sm : g.a_sk)) return 1;
+    if (!gemm_tmap(&tb, g.b, b_kc, g.N, g.K, b_kc ? g.b_sn : g.b_sk)) return 1;
+    static const int st = getenv("LM_GEMM_TMA_ST") ? atoi(getenv("LM_GEMM_TMA_ST")) : 4;
+#define LM_TMA_ST(S)                                                                      \
+    if (st == S) {                                                                        \
+        if (a_kc && b_kc) return launch_dgemm_tma_kernel<true, true, S>(g, ta, tb, grid, s); \
+        if (a_kc) return launch_dgemm_tma_kernel<true, false, S>(g, ta, tb, grid, s);        \
+        if (b_kc) return launch_dgemm_tma_kernel<false, true, S>(g, ta, tb, grid, s);        \
+        return launch_dgemm_tma_kernel<false, false, S>(g, ta, tb, grid, s);                 \
+    }
+    LM_TMA_ST(3)
+    LM_TMA_ST(5)
+    LM_TMA_ST(6)
+#undef LM_TMA_ST
+    if (a_kc && b_kc) return launch_dgemm_tma_kernel<true, true, 4>(g, ta, tb, grid, s);
+    if (a_kc) return launch_dgemm_tma_kernel<true, false, 4>(g, ta, tb, grid, s);
+    if (b_kc) return launch_dgemm_tma_kernel<false, true, 4>(g, ta, tb, grid, s);
+    return launch_dgemm_tma_kernel<false, false, 4>(g, ta, tb, grid, s);
+}
+
 // Few partials: one thread per element, loads unrolled (independent).
 __global__ void __launch_bounds__(256) splitk_finish_flat(const double *__restrict__ part, int64_t M, int64_t N,
                                                           int64_t nz, double *c, int64_t c_sm, int64_t c_sn, int syrk) {
@@ -621,8 +868,11 @@ int dgemm_cfg(GemmArgs &g, bool a_cm, bool b_cn, bool va, bool vb, cudaStream_t 
         g.part = part.as<double>();
     }
     dim3 grid((unsigned)tiles, 1, (unsigned)splits);
-    int rc;
-    if (a_cm && b_cn)
+    int rc = try_launch_dgemm_tma(g, grid, s);
+    if (rc < 0) return rc;
+    if (rc == 0)
+        ;
+    else if (a_cm && b_cn)
         rc = launch_dgemm_layout<true, true, BKT, ST>(g, va, vb, grid, s);
     else if (a_cm)
         rc = launch_dgemm_layout<true, false, BKT, ST>(g, va, vb, grid, s);
