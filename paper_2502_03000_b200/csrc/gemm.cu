@@ -721,7 +721,8 @@ int launch_dgemm_tma_kernel(const GemmArgs &g, const CUtensorMap &ta, const CUte
 
 // 0: launched; 1: not TMA-addressable (the caller launches the cp.async kernel)
 int try_launch_dgemm_tma(const GemmArgs &g, dim3 grid, cudaStream_t s) {
-    if (!gemm_tma_enabled() || g.sub) return 1;  // the LU's C -= A B keeps the tuned cp.async ring
+    static const bool tma_sub = getenv("LM_GEMM_TMA_SUB") && getenv("LM_GEMM_TMA_SUB")[0] == '1';
+    if (!gemm_tma_enabled() || (g.sub && !tma_sub)) return 1;  // the LU's C -= A B keeps the cp.async ring
     const bool a_kc = g.a_sk == 1, b_kc = g.b_sk == 1;
     if (!a_kc && g.a_sm != 1) return 1;
     if (!b_kc && g.b_sn != 1) return 1;
