@@ -799,6 +799,7 @@ int launch_dgemm_kernel(const GemmArgs &g, dim3 grid, cudaStream_t s) {
     if (int rc = func_attrs(k, smem)) return rc;
     LM_CUDA(launch_pdl(k, grid, dim3(kGmThreads), smem, s, g));
     LM_LAUNCHED(1);
+    note_variant("gemm_cp");
     return 0;
 }
 

@@ -118,3 +118,39 @@ def test_batched_lu_variants_bitwise(variant, kernel):
     got = run_lu(variant)
     assert got["variant"] == kernel
     assert got["x"] == ref["x"]
+
+
+GEMM_SCRIPT = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2502_03000_b200 as lm
+from paper_2502_03000_b200 import _native
+rng = np.random.default_rng(31)
+X = lm.DenseMatrix(rng.uniform(-1, 1, (300, 78)))
+Y = lm.DenseMatrix(rng.uniform(-1, 1, (78, 2050)))
+A = lm.DenseMatrix(rng.uniform(-1, 1, (1000, 130)))
+P = lm.evaluate(X * Y).to_numpy()
+v1 = _native.last_variant()
+S = lm.evaluate(A.t() * A).to_numpy()
+print(json.dumps({"P": P.view(np.int64).ravel()[::97].tolist(), "S": S.view(np.int64).ravel()[::13].tolist(),
+                  "variant": v1, "variant_syrk": _native.last_variant()}))
+"""
+
+
+def test_gemm_tma_and_cp_async_kernels_bitwise():
+    """The TMA-fed GEMM/SYRK kernel (default) and the cp.async kernel
+    (LM_GEMM_TMA=0) run the same tiles in the same K order: bit-identical
+    products, edge tiles (300 x 2050, K = 78 / 1000) included."""
+    def run_g(env_extra):
+        env = dict(os.environ)
+        env.update(env_extra)
+        out = subprocess.run([sys.executable, "-c", GEMM_SCRIPT, str(ROOT)], env=env, capture_output=True, text=True,
+                             timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    ref = run_g({})
+    assert ref["variant"] == "gemm_tma" and ref["variant_syrk"] == "gemm_tma"
+    got = run_g({"LM_GEMM_TMA": "0"})
+    assert got["variant"] == "gemm_cp" and got["variant_syrk"] == "gemm_cp"
+    assert got["P"] == ref["P"] and got["S"] == ref["S"]
