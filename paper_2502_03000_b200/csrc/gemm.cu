@@ -511,8 +511,9 @@ __global__ void __launch_bounds__(kGmThreads) dgemm_dmma(GemmArgs g) {
 // engine zero-fills outside the tensor).  Tile layouts in shared memory:
 //   K-contiguous operand (KC): box {16 k, 64 outer}: row o = 128 B (k 0..15),
 //     16-byte chunk c at c ^ (o & 7);
-//   outer-contiguous operand (OC): 4 boxes {16 outer, 16 k}: box q = 2 KB,
-//     row k = 128 B (outer 16q..16q+15), chunk c at c ^ (k & 7).
+//   outer-contiguous operand (OC): 8 boxes {8 outer, 16 k}, no swizzle: box
+//     q = 1 KB, row k = 64 B (outer 8q..8q+7) -- a fragment's 4 consecutive
+//     k rows alternate between the two 64-byte bank halves.
 // Both make the m8n8k4 fragment loads hit the 2-wavefront minimum.  K
 // chunks of a split are multiples of 16, so a box never reads another
 // split's K range; only the tensor's own end is zero-filled.
@@ -520,8 +521,7 @@ constexpr int kTmaTile = BM * BK * 8;  // bytes per operand tile (8 KB)
 
 template <bool KC> __device__ __forceinline__ double tfrag(const unsigned char *t, int o, int k) {
     if (KC) return *reinterpret_cast<const double *>(t + o * 128 + ((((k >> 1) ^ (o & 7))) << 4) + ((k & 1) << 3));
-    return *reinterpret_cast<const double *>(t + ((o >> 4) << 11) + k * 128 + (((((o & 15) >> 1) ^ (k & 7))) << 4) +
-                                             ((o & 1) << 3));
+    return *reinterpret_cast<const double *>(t + ((o >> 3) << 10) + k * 64 + ((o & 7) << 3));
 }
 
 __device__ __forceinline__ unsigned smaddr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -544,11 +544,11 @@ __device__ __forceinline__ void tma_tile(unsigned dst, const CUtensorMap *tm, in
             : "memory");
     } else {
 #pragma unroll
-        for (int q = 0; q < BM / 16; ++q)
+        for (int q = 0; q < BM / 8; ++q)
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-                "[%4];" ::"r"(dst + q * 2048),
-                "l"(tm), "r"((int)(o0 + 16 * q)), "r"((int)k0), "r"(bar)
+                "[%4];" ::"r"(dst + q * 1024),
+                "l"(tm), "r"((int)(o0 + 8 * q)), "r"((int)k0), "r"(bar)
                 : "memory");
     }
 }
@@ -674,8 +674,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 gemm_tmap_encoder() {
 }
 
 // Tensor map of one operand: KC (K unit-stride): dims {K, outer}, box
-// {16, 64}; OC (outer unit-stride): dims {outer, K}, box {16, 16}; 128-byte
-// swizzle.  False when TMA cannot address it (alignment, strides, sizes).
+// {16, 64}, 128-byte swizzle; OC (outer unit-stride): dims {outer, K}, box
+// {8, 16}, no swizzle.  False when TMA cannot address it (alignment, strides, sizes).
 static bool gemm_tmap(CUtensorMap *tm, const double *base, bool kc, int64_t outer, int64_t K, int64_t stride) {
     auto enc = gemm_tmap_encoder();
     if (!enc || ((uintptr_t)base & 15) || (stride * 8) % 16 || stride <= 0 || outer > 0x7fffffff || K > 0x7fffffff ||
@@ -691,12 +691,12 @@ static bool gemm_tmap(CUtensorMap *tm, const double *base, bool kc, int64_t oute
     } else {
         dims[0] = (cuuint64_t)outer;
         dims[1] = (cuuint64_t)K;
-        box[0] = 16;
+        box[0] = 8;
         box[1] = BK;
     }
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               CU_TENSOR_MAP_INTERLEAVE_NONE, kc ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static bool gemm_tma_enabled() {
