@@ -862,6 +862,8 @@ int dgemm_cfg(GemmArgs &g, bool a_cm, bool b_cn, bool va, bool vb, cudaStream_t 
     const int64_t tiles = g.syrk ? tM * (tM + 1) / 2 : tM * tN;
     g.tiles_n = tN;
     int64_t splits = g.sub ? 1 : choose_splits(tiles, M, N, K, BKT, dgemm_resident<BKT, ST>());
+    static const int64_t force_splits = getenv("LM_GEMM_SPLITS") ? atoll(getenv("LM_GEMM_SPLITS")) : 0;  // A/B
+    if (force_splits > 0 && !g.sub && splits > 1) splits = force_splits;
     g.kchunk = ceil_div(ceil_div(K, splits), BKT) * BKT;
     splits = ceil_div(K, g.kchunk);
     Scratch part;
