@@ -25,7 +25,10 @@ the product path always uses the CUDA kernel and the library's NCCL.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import os
+import sys
 
 import torch
 
@@ -92,6 +95,23 @@ def _dist_world(group=None):
     return 0, 1
 
 
+@contextlib.contextmanager
+def _stdout_to_stderr():
+    """NCCL prints its version banner on file descriptor 1 at the first call
+    (e.g. with NCCL_DEBUG=VERSION in the environment); keep the process's
+    stdout -- bench.py's single JSON line -- clean by pointing fd 1 at
+    stderr while NCCL initialises."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    try:
+        os.dup2(2, 1)
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 class NcclComm:
     """An NCCL communicator of the C-ABI (lm_nccl_init_rank), one process
     per GPU.  Rank 0 creates the unique id; with more than one rank it is
@@ -105,7 +125,8 @@ class NcclComm:
         self.rank, self.world = _dist_world(group)
         uid = ctypes.create_string_buffer(128)
         if self.rank == 0:
-            N.check(lib.lm_nccl_unique_id(uid), "lm_nccl_unique_id")
+            with _stdout_to_stderr():
+                N.check(lib.lm_nccl_unique_id(uid), "lm_nccl_unique_id")
         if self.world > 1:
             import torch.distributed as dist
             box = [uid.raw if self.rank == 0 else None]
@@ -113,7 +134,8 @@ class NcclComm:
                                        group=group)
             uid = ctypes.create_string_buffer(box[0], 128)
         self._comm = ctypes.c_void_p()
-        N.check(lib.lm_nccl_init_rank(self.world, self.rank, uid, ctypes.byref(self._comm)), "lm_nccl_init_rank")
+        with _stdout_to_stderr():
+            N.check(lib.lm_nccl_init_rank(self.world, self.rank, uid, ctypes.byref(self._comm)), "lm_nccl_init_rank")
 
     def allreduce_sum(self, t: torch.Tensor) -> torch.Tensor:
         """In-place sum over the ranks, asynchronous on the current stream."""
