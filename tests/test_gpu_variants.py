@@ -108,11 +108,13 @@ def run_lu(env_extra):
 
 
 @pytest.mark.parametrize("variant,kernel", [({"LM_BATCHED_LU": "shift"}, "shift64"),
+                                            ({"LM_BATCHED_LU": "wave"}, "wave64"),
                                             ({"LM_BATCHED_LU": "rows"}, "rows")])
 def test_batched_lu_variants_bitwise(variant, kernel):
-    """Config 4b's kernels: the pivot-free fast path (default) against the
-    round-1 pivoting kernel on every system and the unrolled kernel, on a
-    batch where half the systems pivot: bit-identical solutions."""
+    """Config 4b's kernels: the blocked pivot-free fast path (default)
+    against the unblocked pivot-free wavefront kernel, the round-1 pivoting
+    kernel on every system and the unrolled kernel, on a batch where half
+    the systems pivot: bit-identical solutions."""
     ref = run_lu({})
     assert ref["variant"] == "nopiv64"
     got = run_lu(variant)
