@@ -165,7 +165,12 @@ int lm_set_identity(int dtype, lm_view out, void *stream);
  * per-instance lazymat lu_factor + lu_solve).  x arrives holding b and is
  * overwritten with the solution; A is only read.  Optional outputs (NULL
  * to skip): lu_out (batch*n*n LU factors), d_piv (batch*n pivots).
- * d_info[b] = 0 or failing column + 1. */
+ * d_info[b] = 0 or failing column + 1.  For 32 < n <= 64 without lu_out
+ * this is two launches on `stream`: a pivot-free fast path that proves the
+ * reference keeps every pivot on the diagonal (|multiplier| < 1) and
+ * certifies its quotients, then the pivoting kernel on the systems it
+ * could not prove (it marks them d_info = -1 in between; d_info is final
+ * when the call's work completes). */
 int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void *x, void *lu_out, int64_t *d_piv,
                         int32_t *d_info, void *stream);
 /* lm_lu_solve_batched plus, in the same pass, each instance's R10 structure
@@ -173,7 +178,8 @@ int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void
  * (lbw + ubw <= max(4, n/4)), 2 upper triangular, 3 lower triangular,
  * 4 symmetric.  Every instance is LU-solved; the caller re-solves the
  * band / triangular ones with their own kernels (their LU result and
- * d_info entry are not meaningful).  One kernel, one host read. */
+ * d_info entry are not meaningful).  One pass (two launches for
+ * 32 < n <= 64, as above), one host read. */
 int lm_solve_batched_classified(int dtype, int64_t n, int64_t batch, const void *a, void *x, int32_t *d_cls,
                                 int32_t *d_info, void *stream);
 /* Batched structure classification of `batch` contiguous F-order n x n
