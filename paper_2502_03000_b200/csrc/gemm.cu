@@ -534,9 +534,9 @@ __device__ __forceinline__ void tma_wait(unsigned bar, unsigned parity) {
         : "memory");
 }
 
-template <bool KC>
+template <bool KC, int OUTER>
 __device__ __forceinline__ void tma_tile(unsigned dst, const CUtensorMap *tm, int64_t o0, int64_t k0, unsigned bar) {
-    if (KC) {
+    if (KC) {  // one box {16 k, OUTER rows}
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
                 "r"(dst),
@@ -544,7 +544,7 @@ __device__ __forceinline__ void tma_tile(unsigned dst, const CUtensorMap *tm, in
             : "memory");
     } else {
 #pragma unroll
-        for (int q = 0; q < BM / 8; ++q)
+        for (int q = 0; q < OUTER / 8; ++q)
             asm volatile(
                 "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
                 "[%4];" ::"r"(dst + q * 1024),
@@ -553,19 +553,24 @@ __device__ __forceinline__ void tma_tile(unsigned dst, const CUtensorMap *tm, in
     }
 }
 
-// Warp-specialised: 4 MMA warps (2 x 2, warp tile 32 x 32) and one producer
-// warp; stages are handed over with full / empty mbarriers only -- no
-// CTA-wide barrier per K step (a __syncthreads every 64 DMMAs per warp lines
-// the warps up on the DMMA latency, tools/dmma_occ_probe.cu).
+// Warp-specialised: 4 MMA warps (2 x 2) and one producer warp; stages are
+// handed over with full / empty mbarriers only -- no CTA-wide barrier per K
+// step (a __syncthreads every 64 DMMAs per warp lines the warps up on the
+// DMMA latency, tools/dmma_occ_probe.cu).  The CTA tile is 64 x BNT: BNT =
+// 64 (warp tile 32 x 32), or 128 for products 65..128 columns wide (warp
+// tile 32 x 64: a 100-wide product is one tile column instead of two 64-wide
+// ones); 8 x 8 fragments wholly outside C are skipped (warp-uniform).
 constexpr int kGmTmaThreads = kGmThreads + 32;
-template <bool A_KC, bool B_KC, int ST>
-__global__ void __launch_bounds__(kGmTmaThreads) dgemm_dmma_tma(GemmArgs g, const __grid_constant__ CUtensorMap tmA,
+template <bool A_KC, bool B_KC, int ST, int BNT>
+__global__ void __launch_bounds__(kGmTmaThreads, BNT == 64 ? 1 : 2) dgemm_dmma_tma(GemmArgs g, const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB) {
+    constexpr int NFW = BNT / 16;                    // N fragments per warp
+    constexpr int TA = kTmaTile, TB = BNT * BK * 8;  // stage bytes per operand
     pdl_wait();  // inputs may be the previous kernel's output (PDL)
     pdl_trigger();
     extern __shared__ unsigned char tsm_raw[];
     unsigned char *tsm = tsm_raw + ((1024 - (smaddr(tsm_raw) & 1023)) & 1023);  // 128B swizzle: 1 KB aligned
-    unsigned long long *full = reinterpret_cast<unsigned long long *>(tsm + ST * 2 * kTmaTile);
+    unsigned long long *full = reinterpret_cast<unsigned long long *>(tsm + ST * (TA + TB));
     unsigned long long *empty = full + ST;
     int64_t tm, tn;
     if (g.syrk) {
@@ -579,7 +584,7 @@ __global__ void __launch_bounds__(kGmTmaThreads) dgemm_dmma_tma(GemmArgs g, cons
         tm = blockIdx.x % ((g.M + BM - 1) / BM);
         tn = blockIdx.x / ((g.M + BM - 1) / BM);
     }
-    const int64_t m0 = tm * BM, n0 = tn * BN;
+    const int64_t m0 = tm * BM, n0 = tn * BNT;
     const int64_t kb = (int64_t)blockIdx.z * g.kchunk;
     int64_t ke = kb + g.kchunk;
     if (ke > g.K) ke = g.K;
@@ -600,38 +605,47 @@ __global__ void __launch_bounds__(kGmTmaThreads) dgemm_dmma_tma(GemmArgs g, cons
                 const int s = (int)(it % ST);
                 if (it >= ST) tma_wait(smaddr(&empty[s]), (unsigned)(((it / ST) - 1) & 1));
                 const unsigned bar = smaddr(&full[s]);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2u * kTmaTile)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((unsigned)(TA + TB))
                              : "memory");
                 const int64_t k0 = kb + it * BK;
-                tma_tile<A_KC>(smaddr(tsm + s * 2 * kTmaTile), &tmA, m0, k0, bar);
-                tma_tile<B_KC>(smaddr(tsm + s * 2 * kTmaTile + kTmaTile), &tmB, n0, k0, bar);
+                tma_tile<A_KC, BM>(smaddr(tsm + s * (TA + TB)), &tmA, m0, k0, bar);
+                tma_tile<B_KC, BNT>(smaddr(tsm + s * (TA + TB) + TA), &tmB, n0, k0, bar);
             }
         }
         return;
     }
-    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * (BNT / 2);
     const int fr = lane >> 2, fc = lane & 3;
-    double acc[4][4][2];
+    double acc[4][NFW][2];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NFW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // live fragment rows / columns (warp-uniform)
+    unsigned live_i = 0, live_j = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (m0 + wm + i * 8 < g.M) live_i |= 1u << i;
+#pragma unroll
+    for (int j = 0; j < NFW; ++j)
+        if (n0 + wn + j * 8 < g.N) live_j |= 1u << j;
     for (int64_t it = 0; it < nk; ++it) {
         const int s = (int)(it % ST);
         tma_wait(smaddr(&full[s]), (unsigned)((it / ST) & 1));
-        const unsigned char *a_s = tsm + s * 2 * kTmaTile;
-        const unsigned char *b_s = a_s + kTmaTile;
+        const unsigned char *a_s = tsm + s * (TA + TB);
+        const unsigned char *b_s = a_s + TA;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
-            double af[4], bf[4];
+            double af[4], bf[NFW];
 #pragma unroll
             for (int i = 0; i < 4; ++i) af[i] = tfrag<A_KC>(a_s, wm + i * 8 + fr, kk + fc);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bf[j] = tfrag<B_KC>(b_s, wn + j * 8 + fr, kk + fc);
+            for (int j = 0; j < NFW; ++j) bf[j] = tfrag<B_KC>(b_s, wn + j * 8 + fr, kk + fc);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+                for (int j = 0; j < NFW; ++j)
+                    if (BNT == 64 || (((live_i >> i) & (live_j >> j)) & 1)) dmma(acc[i][j], af[i], bf[j]);
         }
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smaddr(&empty[s])) : "memory");
@@ -640,7 +654,7 @@ __global__ void __launch_bounds__(kGmTmaThreads) dgemm_dmma_tma(GemmArgs g, cons
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NFW; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const int64_t m = m0 + wm + i * 8 + fr, n = n0 + wn + j * 8 + 2 * fc + h;
@@ -676,7 +690,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 gemm_tmap_encoder() {
 // Tensor map of one operand: KC (K unit-stride): dims {K, outer}, box
 // {16, 64}, 128-byte swizzle; OC (outer unit-stride): dims {outer, K}, box
 // {8, 16}, no swizzle.  False when TMA cannot address it (alignment, strides, sizes).
-static bool gemm_tmap(CUtensorMap *tm, const double *base, bool kc, int64_t outer, int64_t K, int64_t stride) {
+static bool gemm_tmap(CUtensorMap *tm, const double *base, bool kc, int64_t outer, int64_t K, int64_t stride,
+                      int box_outer = BM) {
     auto enc = gemm_tmap_encoder();
     if (!enc || ((uintptr_t)base & 15) || (stride * 8) % 16 || stride <= 0 || outer > 0x7fffffff || K > 0x7fffffff ||
         stride * 8 >= (1ll << 40))
@@ -687,7 +702,7 @@ static bool gemm_tmap(CUtensorMap *tm, const double *base, bool kc, int64_t oute
         dims[0] = (cuuint64_t)K;
         dims[1] = (cuuint64_t)outer;
         box[0] = BK;
-        box[1] = BM;
+        box[1] = (cuuint32_t)box_outer;
     } else {
         dims[0] = (cuuint64_t)outer;
         dims[1] = (cuuint64_t)K;
@@ -707,20 +722,20 @@ static bool gemm_tma_enabled() {
     return on;
 }
 
-template <bool A_KC, bool B_KC, int ST>
+template <bool A_KC, bool B_KC, int ST, int BNT>
 int launch_dgemm_tma_kernel(const GemmArgs &g, const CUtensorMap &ta, const CUtensorMap &tb, dim3 grid,
                             cudaStream_t s) {
-    auto k = dgemm_dmma_tma<A_KC, B_KC, ST>;
-    constexpr int smem = ST * 2 * kTmaTile + 1024 + 16 * ST;
+    auto k = dgemm_dmma_tma<A_KC, B_KC, ST, BNT>;
+    constexpr int smem = ST * (kTmaTile + BNT * BK * 8) + 1024 + 16 * ST;
     if (int rc = func_attrs(k, smem)) return rc;
     LM_CUDA(launch_pdl(k, grid, dim3(kGmTmaThreads), smem, s, g, ta, tb));
     LM_LAUNCHED(1);
-    note_variant("gemm_tma");
+    note_variant(BNT == 64 ? "gemm_tma" : "gemm_tma_wide");
     return 0;
 }
 
 // 0: launched; 1: not TMA-addressable (the caller launches the cp.async kernel)
-int try_launch_dgemm_tma(const GemmArgs &g, dim3 grid, cudaStream_t s) {
+int try_launch_dgemm_tma(const GemmArgs &g, dim3 grid, cudaStream_t s, bool wide) {
     static const bool tma_sub = getenv("LM_GEMM_TMA_SUB") && getenv("LM_GEMM_TMA_SUB")[0] == '1';
     if (!gemm_tma_enabled() || (g.sub && !tma_sub)) return 1;  // the LU's C -= A B keeps the cp.async ring
     const bool a_kc = g.a_sk == 1, b_kc = g.b_sk == 1;
@@ -728,23 +743,31 @@ int try_launch_dgemm_tma(const GemmArgs &g, dim3 grid, cudaStream_t s) {
     if (!b_kc && g.b_sn != 1) return 1;
     CUtensorMap ta, tb;
     if (!gemm_tmap(&ta, g.a, a_kc, g.M, g.K, a_kc ? g.a_sm : g.a_sk)) return 1;
-    if (!gemm_tmap(&tb, g.b, b_kc, g.N, g.K, b_kc ? g.b_sn : g.b_sk)) return 1;
-    static const int st = getenv("LM_GEMM_TMA_ST") ? atoi(getenv("LM_GEMM_TMA_ST")) : 4;
-#define LM_TMA_ST(S)                                                                      \
-    if (st == S) {                                                                        \
-        if (a_kc && b_kc) return launch_dgemm_tma_kernel<true, true, S>(g, ta, tb, grid, s); \
-        if (a_kc) return launch_dgemm_tma_kernel<true, false, S>(g, ta, tb, grid, s);        \
-        if (b_kc) return launch_dgemm_tma_kernel<false, true, S>(g, ta, tb, grid, s);        \
-        return launch_dgemm_tma_kernel<false, false, S>(g, ta, tb, grid, s);                 \
+    if (!gemm_tmap(&tb, g.b, b_kc, g.N, g.K, b_kc ? g.b_sn : g.b_sk, wide ? 128 : BM)) return 1;
+    if (wide) {
+        if (a_kc && b_kc) return launch_dgemm_tma_kernel<true, true, 4, 128>(g, ta, tb, grid, s);
+        if (a_kc) return launch_dgemm_tma_kernel<true, false, 4, 128>(g, ta, tb, grid, s);
+        if (b_kc) return launch_dgemm_tma_kernel<false, true, 4, 128>(g, ta, tb, grid, s);
+        return launch_dgemm_tma_kernel<false, false, 4, 128>(g, ta, tb, grid, s);
     }
-    LM_TMA_ST(3)
-    LM_TMA_ST(5)
-    LM_TMA_ST(6)
-#undef LM_TMA_ST
-    if (a_kc && b_kc) return launch_dgemm_tma_kernel<true, true, 4>(g, ta, tb, grid, s);
-    if (a_kc) return launch_dgemm_tma_kernel<true, false, 4>(g, ta, tb, grid, s);
-    if (b_kc) return launch_dgemm_tma_kernel<false, true, 4>(g, ta, tb, grid, s);
-    return launch_dgemm_tma_kernel<false, false, 4>(g, ta, tb, grid, s);
+    if (a_kc && b_kc) return launch_dgemm_tma_kernel<true, true, 4, 64>(g, ta, tb, grid, s);
+    if (a_kc) return launch_dgemm_tma_kernel<true, false, 4, 64>(g, ta, tb, grid, s);
+    if (b_kc) return launch_dgemm_tma_kernel<false, true, 4, 64>(g, ta, tb, grid, s);
+    return launch_dgemm_tma_kernel<false, false, 4, 64>(g, ta, tb, grid, s);
+}
+
+// Whether a product takes the 64 x 128-tile TMA kernel: 65..128 columns
+// (one tile column instead of two), not SYRK / the LU's update, and TMA-
+// addressable operands (checked again by try_launch_dgemm_tma); opt-in.
+static bool dgemm_wide(const GemmArgs &g) {
+    // opt-in (LM_GEMM_WIDE=1): measured slower on config 3b (50 vs 33 us per
+    // step: 2 CTAs per SM at 168 registers with spills, twice the per-CTA work)
+    static const bool on = getenv("LM_GEMM_WIDE") && getenv("LM_GEMM_WIDE")[0] == '1';
+    if (!on || !gemm_tma_enabled() || g.syrk || g.sub || g.N <= 64 || g.N > 128) return false;
+    const bool a_kc = g.a_sk == 1, b_kc = g.b_sk == 1;
+    const int64_t sa = a_kc ? g.a_sm : g.a_sk, sb = b_kc ? g.b_sn : g.b_sk;
+    return (a_kc || g.a_sm == 1) && (b_kc || g.b_sn == 1) && ((uintptr_t)g.a & 15) == 0 &&
+           ((uintptr_t)g.b & 15) == 0 && sa % 2 == 0 && sb % 2 == 0;
 }
 
 // Few partials: one thread per element, loads unrolled (independent).
@@ -858,7 +881,8 @@ inline int64_t choose_splits(int64_t tiles, int64_t M, int64_t N, int64_t K, int
 template <int BKT, int ST>
 int dgemm_cfg(GemmArgs &g, bool a_cm, bool b_cn, bool va, bool vb, cudaStream_t s) {
     const int64_t M = g.M, N = g.N, K = g.K;
-    const int64_t tM = ceil_div(M, BM), tN = ceil_div(N, BN);
+    const bool wide = dgemm_wide(g);
+    const int64_t tM = ceil_div(M, BM), tN = wide ? 1 : ceil_div(N, BN);
     const int64_t tiles = g.syrk ? tM * (tM + 1) / 2 : tM * tN;
     g.tiles_n = tN;
     int64_t splits = g.sub ? 1 : choose_splits(tiles, M, N, K, BKT, dgemm_resident<BKT, ST>());
@@ -872,8 +896,9 @@ int dgemm_cfg(GemmArgs &g, bool a_cm, bool b_cn, bool va, bool vb, cudaStream_t 
         g.part = part.as<double>();
     }
     dim3 grid((unsigned)tiles, 1, (unsigned)splits);
-    int rc = try_launch_dgemm_tma(g, grid, s);
+    int rc = try_launch_dgemm_tma(g, grid, s, wide);
     if (rc < 0) return rc;
+    LM_REQUIRE(rc == 0 || !wide, "gemm: wide tile chosen for operands TMA cannot address");
     if (rc == 0)
         ;
     else if (a_cm && b_cn)

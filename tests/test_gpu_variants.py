@@ -156,3 +156,32 @@ def test_gemm_tma_and_cp_async_kernels_bitwise():
     got = run_g({"LM_GEMM_TMA": "0"})
     assert got["variant"] == "gemm_cp" and got["variant_syrk"] == "gemm_cp"
     assert got["P"] == ref["P"] and got["S"] == ref["S"]
+
+
+def test_gemm_wide_tile_kernel_bitwise():
+    """The opt-in 64 x 128-tile TMA kernel (LM_GEMM_WIDE=1) on a product
+    100 columns wide agrees with the default kernel normwise to 1e-12 (the
+    split-K grouping follows the tile count, so the sums may associate
+    differently)."""
+    script = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2502_03000_b200 as lm
+from paper_2502_03000_b200 import _native
+rng = np.random.default_rng(32)
+X = lm.DenseMatrix(rng.uniform(-1, 1, (1000, 300)))
+T = lm.DenseMatrix(rng.uniform(-1, 1, (300, 100)))
+P = lm.evaluate(X * T).to_numpy()
+print(json.dumps({"P": P.ravel()[::31].tolist(), "variant": _native.last_variant()}))
+"""
+    outs = []
+    for env_extra in ({}, {"LM_GEMM_WIDE": "1"}):
+        env = dict(os.environ)
+        env.update(env_extra)
+        out = subprocess.run([sys.executable, "-c", script, str(ROOT)], env=env, capture_output=True, text=True,
+                             timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs.append(json.loads(out.stdout.strip().splitlines()[-1]))
+    assert outs[0]["variant"] == "gemm_tma" and outs[1]["variant"] == "gemm_tma_wide"
+    assert close(outs[1]["P"], outs[0]["P"], 1e-12)
