@@ -855,7 +855,11 @@ __device__ __forceinline__ void named_barrier(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
-__global__ void __launch_bounds__(WS_THREADS, 1) atb_schur_trace_stream_ws(int64_t batch, const double *__restrict__ A,
+// MW MMA warps: 16 (warp tile 32 x 32, the round-1 layout) or 8 (warp tile
+// 64 x 32: 12 instead of 16 fragment loads per 32 DMMAs -- a quarter less
+// shared-memory traffic per flop at the board's power cap).
+template <int MW>
+__global__ void __launch_bounds__(32 * (MW + WS_EPI_WARPS), 1) atb_schur_trace_stream_ws(int64_t batch, const double *__restrict__ A,
                                                                         const double *__restrict__ C,
                                                                         const double *__restrict__ D,
                                                                         double *__restrict__ E, double *__restrict__ S,
@@ -872,15 +876,18 @@ __global__ void __launch_bounds__(WS_THREADS, 1) atb_schur_trace_stream_ws(int64
 #pragma unroll
         for (int q = 0; q < TST4; ++q) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.full[q])), "r"(1));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.empty[q])), "r"(WS_MMA_WARPS));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(&sm.empty[q])), "r"(MW));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    if (warp < WS_MMA_WARPS) {
+    constexpr int TH = 32 * (MW + WS_EPI_WARPS);
+    constexpr int MF = MW == 16 ? 4 : 8;  // M fragments per warp
+    constexpr int WMR = HN / (8 * MF);    // warps along M
+    if (warp < MW) {
         // ---------------- MMA warps: DMMA, trace terms, the TMA ring ----------------
-        const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+        const int wm = (warp % WMR) * (8 * MF), wn = (warp / WMR) * 32;
         const int fr = lane >> 2, fc = lane & 3;
         // half-warp conflict-free fragment rows (see atb_schur_trace_stream_tma)
         auto perm = [](int r) { return (r & 1) | ((r & 2) << 1) | ((r & 4) >> 1); };
@@ -915,39 +922,44 @@ __global__ void __launch_bounds__(WS_THREADS, 1) atb_schur_trace_stream_ws(int64
         if (lane == 0 && warp < TST4 - 1 && warp < total) produce(warp);
         int64_t gch = 0;
         for (int64_t j = 0; j < J; ++j) {
-            double acc[4][4][2];
+            double acc[MF][4][2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < MF; ++i)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) acc[i][q][0] = acc[i][q][1] = 0.0;
             double tr = 0.0;
             for (int c = 0; c < NCH; ++c, ++gch) {
                 const int buf = (int)(gch % TST4);
-                if (lane == 0 && warp == (int)(gch % WS_MMA_WARPS) && gch + TST4 - 1 < total) produce(gch + TST4 - 1);
+                if (lane == 0 && warp == (int)(gch % MW) && gch + TST4 - 1 < total) produce(gch + TST4 - 1);
                 __syncwarp();
                 mbar_wait(&sm.full[buf], (unsigned)((gch / TST4) & 1));
                 const double *as = sm.a[buf];
                 const double *bs = sm.b[buf];
 #pragma unroll
                 for (int kk = 0; kk < TKC8; kk += 4) {
-                    double af[4], bf[4];
+                    double af[MF], bf[4];
                     const int o = kk ? sw4 : sw0;
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + pr) * TKC8 + o];
+                    for (int i = 0; i < MF; ++i) af[i] = as[(wm + i * 8 + pr) * TKC8 + o];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) bf[q] = bs[(wn + q * 8 + pr) * TKC8 + o];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < MF; ++i)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) dmma884(acc[i][q], af[i], bf[q]);
                 }
                 {
                     // trace terms: sum_{k in chunk} sum_i A(i,k) B(k,i); 2 per thread
                     const double *ac = sm.ac[buf];
-                    const int i = tid & 127, k2 = (tid >> 7) * 2;
-                    const int bo = i * TKC8 + (((k2 >> 1) ^ ((i >> 1) & 3)) << 1);  // k2 even
-                    tr = fma(ac[k2 * HN + i], bs[bo], tr);
-                    tr = fma(ac[(k2 + 1) * HN + i], bs[bo + 1], tr);
+                    constexpr int KPT = 32 / MW;  // trace k values per thread (8 per chunk over 32*MW threads)
+                    const int i = tid & 127;
+#pragma unroll
+                    for (int u = 0; u < KPT; u += 2) {
+                        const int k2 = (tid >> 7) * KPT + u;
+                        const int bo = i * TKC8 + (((k2 >> 1) ^ ((i >> 1) & 3)) << 1);  // k2 even
+                        tr = fma(ac[k2 * HN + i], bs[bo], tr);
+                        tr = fma(ac[(k2 + 1) * HN + i], bs[bo + 1], tr);
+                    }
                 }
                 __syncwarp();
                 if (lane == 0)
@@ -955,21 +967,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1) atb_schur_trace_stream_ws(int64
             }
             tr = warp_sum(tr);
             if (lane == 0) sm.red[j & 1][warp] = tr;
-            named_barrier(1, WS_THREADS);  // B1: the epilogue warps are done with P_{j-1}
+            named_barrier(1, TH);  // B1: the epilogue warps are done with P_{j-1}
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < MF; ++i)
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
                         sm.p[(wn + q * 8 + perm(2 * fc + u)) * SLDP + wm + i * 8 + pr] = acc[i][q][u];
-            named_barrier(2, WS_THREADS);  // B2: P_j and the trace partials complete
+            named_barrier(2, TH);  // B2: P_j and the trace partials complete
         }
         return;
     }
 
     // ---------------- epilogue warps: E_{j-1} = P + C % D during instance j ----------------
-    const int et = tid - 32 * WS_MMA_WARPS;
+    const int et = tid - 32 * MW;
     // slice c of an instance: elements c*1024 + 2*et + 256*r, r < 4
     // (column-major; a warp covers 512 contiguous bytes per r)
     auto load_cd = [&](int64_t bl, int c, double2 (&cv)[4], double2 (&dv)[4]) {
@@ -1007,12 +1019,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1) atb_schur_trace_stream_ws(int64
     for (int64_t j = 0; j < J; ++j) {
         const int64_t b = blockIdx.x + j * G;
         if (j > 0) finish(b - G);
-        named_barrier(1, WS_THREADS);  // B1
-        named_barrier(2, WS_THREADS);  // B2
+        named_barrier(1, TH);  // B1
+        named_barrier(2, TH);  // B2
         if (et == 0) {
             double t = sm.red[j & 1][0];
 #pragma unroll
-            for (int w = 1; w < WS_MMA_WARPS; ++w) t = radd(t, sm.red[j & 1][w]);
+            for (int w = 1; w < MW; ++w) t = radd(t, sm.red[j & 1][w]);
             S[b] = t;
         }
     }
@@ -2191,14 +2203,17 @@ int launch_stream_ws(int64_t batch, const double *a, const double *b, const doub
                      double *s, cudaStream_t st) {
     CUtensorMap ta, tb;
     if (batch * HN > 0x7fffffff || !rows_tensor_map(&ta, a, batch) || !rows_tensor_map(&tb, b, batch)) return 1;
-    auto kern = atb_schur_trace_stream_ws;
+    // LM_5A_MW=8: eight MMA warps with 64 x 32 warp tiles (default 16 x 32 x 32)
+    static const int mw = getenv("LM_5A_MW") ? atoi(getenv("LM_5A_MW")) : 16;
+    auto kern = mw == 8 ? atb_schur_trace_stream_ws<8> : atb_schur_trace_stream_ws<16>;
+    const int threads = 32 * ((mw == 8 ? 8 : 16) + WS_EPI_WARPS);
     const size_t smem = sizeof(SmemStreamW) + 512;  // + alignment slack
     if (int rc = func_attrs(kern, smem)) return rc;
-    const int grid = num_sms();  // one 20-warp CTA per SM
+    const int grid = num_sms();  // one CTA per SM
     const int64_t g = batch < grid ? batch : grid;
-    kern<<<(unsigned)g, WS_THREADS, smem, st>>>(batch, a, c, d, e, s, ta, tb);
+    kern<<<(unsigned)g, threads, smem, st>>>(batch, a, c, d, e, s, ta, tb);
     LM_LAUNCHED(1);
-    note_variant("stream_ws");
+    note_variant(mw == 8 ? "stream_ws8" : "stream_ws");
     return 0;
 }
 

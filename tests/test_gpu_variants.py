@@ -50,6 +50,7 @@ def close(a, b, tol):
 
 
 @pytest.mark.parametrize("variant,kernel", [({"LM_5A_TM": "1"}, "stream_tm"), ({"LM_5A_WS": "0"}, "stream_tma"),
+                                            ({"LM_5A_MW": "8"}, "stream_ws8"),
                                             ({"LM_5A_TMA": "0"}, "stream"), ({"LM_5A_STREAM": "0"}, "half")])
 def test_f64_variants_agree(variant, kernel):
     ref = run({}, "f64")
