@@ -218,10 +218,9 @@ __global__ void __launch_bounds__(N) lu_batched_rows(int64_t n, int64_t batch, c
 // (U[k, k:]) for the back sweep (:254-258), which one warp runs with
 // shuffles instead of block barriers.
 template <int N, int KB, bool CLASSIFY>
-__global__ void __launch_bounds__(N, N == 64 ? 6 : 1)
-    lu_batched_shift(int64_t n, int64_t batch, const double *__restrict__ A, double *__restrict__ X,
-                     int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls,
-                     int redo_only) {
+__device__ __forceinline__ void shift_system(const int64_t b, int64_t n, const double *__restrict__ A,
+                                             double *__restrict__ X, int64_t *__restrict__ piv,
+                                             int32_t *__restrict__ info, int32_t *__restrict__ cls) {
     constexpr int W = N / 32 > 0 ? N / 32 : 1;  // warps per system
     constexpr int R = (N + 31) / 32;            // back-sweep positions per lane
     constexpr unsigned MASK = N >= 32 ? 0xffffffffu : ((1u << N) - 1u);
@@ -234,8 +233,6 @@ __global__ void __launch_bounds__(N, N == 64 ? 6 : 1)
     __shared__ int s_fail;
 
     const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-    const int64_t b = blockIdx.x;
-    if (redo_only && info[b] != -1) return;  // after the pivot-free fast path: only the systems it could not prove
     const double *Ab = A + b * n * n;
     double r[N];
 #pragma unroll
@@ -399,6 +396,24 @@ __global__ void __launch_bounds__(N, N == 64 ? 6 : 1)
         if (q * 32 + lane < n) X[b * n + q * 32 + lane] = c[q];
 }
 
+// One system per CTA, or (redo_list set) a small grid that solves exactly the
+// systems the pivot-free fast path listed as unproved.
+template <int N, int KB, bool CLASSIFY>
+__global__ void __launch_bounds__(N, N == 64 ? 6 : 1)
+    lu_batched_shift(int64_t n, int64_t batch, const double *__restrict__ A, double *__restrict__ X,
+                     int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls,
+                     const int *__restrict__ redo_list, const int *__restrict__ redo_count) {
+    if (!redo_list) {
+        shift_system<N, KB, CLASSIFY>(blockIdx.x, n, A, X, piv, info, cls);
+        return;
+    }
+    const int cnt = *redo_count;
+    for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
+        shift_system<N, KB, CLASSIFY>(redo_list[i], n, A, X, piv, info, cls);
+        __syncthreads();  // shared buffers are reused by the next system
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Pivot-free blocked fast path for 32 < n <= 64 (config 4b), bit-identical
 // to _lu_factor + _lu_solve_inplace (lazymat/_loops.py:200-259) whenever
@@ -492,7 +507,7 @@ template <bool CLASSIFY, bool TRACE = false>
 __global__ void __launch_bounds__(64, 6)
     lu_batched_nopiv(int64_t n, int64_t batch, const double *__restrict__ A, double *__restrict__ X,
                      int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls,
-                     long long *__restrict__ trace = nullptr) {
+                     int *__restrict__ redo_list, int *__restrict__ redo_count, long long *__restrict__ trace = nullptr) {
     constexpr int N = 64, KB = 8, NB = N / KB;
     constexpr int UW = N - KB + 2;  // rest width incl. the right-hand side, even
     constexpr unsigned MASK = 0xffffffffu;
@@ -668,7 +683,10 @@ __global__ void __launch_bounds__(64, 6)
         }
     }
     if (__syncthreads_or(bad)) {  // pivoting could swap somewhere: the pivoting kernel redoes this system
-        if (t == 0) info[b] = -1;
+        if (t == 0) {
+            info[b] = -1;
+            redo_list[atomicAdd(redo_count, 1)] = (int)b;
+        }
         return;
     }
     // back sweep (lazymat/_loops.py:254-258), blocked: thread t owns
@@ -712,7 +730,10 @@ __global__ void __launch_bounds__(64, 6)
         }
     }
     if (__syncthreads_or(bad)) {  // an uncertified quotient: the pivoting kernel redoes the system
-        if (t == 0) info[b] = -1;
+        if (t == 0) {
+            info[b] = -1;
+            redo_list[atomicAdd(redo_count, 1)] = (int)b;
+        }
         return;
     }
     LU4B_MARK(26)
@@ -742,7 +763,8 @@ __global__ void __launch_bounds__(64, 6)
 template <bool CLASSIFY>
 __global__ void __launch_bounds__(64, 6)
     lu_batched_wave(int64_t n, int64_t batch, const double *__restrict__ A, double *__restrict__ X,
-                    int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls) {
+                    int64_t *__restrict__ piv, int32_t *__restrict__ info, int32_t *__restrict__ cls,
+                    int *__restrict__ redo_list, int *__restrict__ redo_count) {
     constexpr int N = 64, KB = 8;
     constexpr unsigned MASK = 0xffffffffu;
     constexpr size_t SAT = CLASSIFY ? sizeof(double) * N * (N + 1) : 0;
@@ -858,7 +880,10 @@ __global__ void __launch_bounds__(64, 6)
         }
     }
     if (__syncthreads_or(bad)) {  // pivoting could swap somewhere: the pivoting kernel redoes this system
-        if (t == 0) info[b] = -1;
+        if (t == 0) {
+            info[b] = -1;
+            redo_list[atomicAdd(redo_count, 1)] = (int)b;
+        }
         return;
     }
     // back sweep (lazymat/_loops.py:254-258): thread t holds position t
@@ -904,7 +929,10 @@ __global__ void __launch_bounds__(64, 6)
         }
     }
     if (__syncthreads_or(bad)) {  // an uncertified quotient: the pivoting kernel redoes the system
-        if (t == 0) info[b] = -1;
+        if (t == 0) {
+            info[b] = -1;
+            redo_list[atomicAdd(redo_count, 1)] = (int)b;
+        }
         return;
     }
     if (t == 0) info[b] = 0;
@@ -950,35 +978,40 @@ template <bool CLASSIFY>
 static int launch_batched(int64_t n, int64_t batch, const double *A, double *X, double *LU, int64_t *d_piv,
                           int32_t *d_info, int32_t *d_cls, cudaStream_t s) {
     const int choice = batched_kernel_choice();
-    if (LU == nullptr && n > 32 && choice == 3) {
-        lu_batched_wave<CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls);
+    if (LU == nullptr && n > 32 && (choice == 0 || choice == 3)) {
+        // the fast path lists the systems it cannot prove; a small grid of
+        // the pivoting kernel then solves exactly those
+        Scratch redo;
+        if (int rc = redo.alloc(sizeof(int) * (size_t)(batch + 1), s)) return rc;
+        int *cnt = redo.as<int>(), *list = cnt + 1;
+        LM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), s));
+        if (choice == 3) {
+            lu_batched_wave<CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, list, cnt);
+            note_variant("wave64");
+        } else {
+            long long *trace = lu4b_trace_buffer();
+            if (trace && batch <= 65536)
+                lu_batched_nopiv<CLASSIFY, true>
+                    <<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, list, cnt, trace);
+            else
+                lu_batched_nopiv<CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, list, cnt);
+            note_variant("nopiv64");
+        }
         static const bool noredo = getenv("LM_4B_NOREDO") != nullptr;  // diagnostics: leave info = -1 visible
-        if (!noredo)
-            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 1);
-        note_variant("wave64");
-        LM_LAUNCHED(2);
-        return 0;
-    }
-    if (LU == nullptr && n > 32 && choice == 0) {
-        long long *trace = lu4b_trace_buffer();
-        if (trace && batch <= 65536)
-            lu_batched_nopiv<CLASSIFY, true><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, trace);
-        else
-            lu_batched_nopiv<CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls);
-        static const bool noredo = getenv("LM_4B_NOREDO") != nullptr;  // diagnostics: leave info = -1 visible
-        if (!noredo)
-            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 1);
-        note_variant("nopiv64");
+        if (!noredo) {
+            const int64_t g = batch < 6 * (int64_t)num_sms() ? batch : 6 * (int64_t)num_sms();
+            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)g, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, list, cnt);
+        }
         LM_LAUNCHED(2);
         return 0;
     }
     if (LU == nullptr && choice <= 1) {
         if (n <= 16)
-            lu_batched_shift<16, 8, CLASSIFY><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 0);
+            lu_batched_shift<16, 8, CLASSIFY><<<(unsigned)batch, 16, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, nullptr, nullptr);
         else if (n <= 32)
-            lu_batched_shift<32, 8, CLASSIFY><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 0);
+            lu_batched_shift<32, 8, CLASSIFY><<<(unsigned)batch, 32, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, nullptr, nullptr);
         else
-            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, 0);
+            lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, nullptr, nullptr);
         note_variant(n > 32 ? "shift64" : "shift");
     } else {
         if (n <= 16)
