@@ -989,6 +989,9 @@ static int launch_batched(int64_t n, int64_t batch, const double *A, double *X, 
             lu_batched_wave<CLASSIFY><<<(unsigned)batch, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, list, cnt);
             note_variant("wave64");
         } else {
+            // six 64-thread systems per SM need ~200 KB of shared memory: ask
+            // for the largest carveout (the default one fits fewer CTAs)
+            if (int rc = func_attrs(lu_batched_nopiv<CLASSIFY>, 0, 100)) return rc;
             long long *trace = lu4b_trace_buffer();
             if (trace && batch <= 65536)
                 lu_batched_nopiv<CLASSIFY, true>
@@ -999,6 +1002,7 @@ static int launch_batched(int64_t n, int64_t batch, const double *A, double *X, 
         }
         static const bool noredo = getenv("LM_4B_NOREDO") != nullptr;  // diagnostics: leave info = -1 visible
         if (!noredo) {
+            if (int rc = func_attrs(lu_batched_shift<64, 8, CLASSIFY>, 0, 100)) return rc;
             const int64_t g = batch < 6 * (int64_t)num_sms() ? batch : 6 * (int64_t)num_sms();
             lu_batched_shift<64, 8, CLASSIFY><<<(unsigned)g, 64, 0, s>>>(n, batch, A, X, d_piv, d_info, d_cls, list, cnt);
         }
