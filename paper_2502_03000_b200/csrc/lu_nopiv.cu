@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb
         if (tx < nb && c < nb) a[c * LDD + tx] = A[tx + (int64_t)c * lda];
     __syncthreads();
     for (int k = 0; k < nb; ++k) {
-        const double p = a[k * LDD + k];
-        if (ty == 0 && tx > k && tx < nb) a[k * LDD + tx] /= p;  // multipliers l_ik
+        const double rp = __drcp_rn(a[k * LDD + k]);  // tensor mode: multiply by the reciprocal
+        if (ty == 0 && tx > k && tx < nb) a[k * LDD + tx] *= rp;  // multipliers l_ik
         __syncthreads();
         if (tx > k && tx < nb) {
             const double l = a[k * LDD + tx];
@@ -102,11 +102,14 @@ constexpr int kTriSmem = 2 * NBD * LDD * (int)sizeof(double);
 // x U = a:  x_i = s_i / u_ii;  s_j -= x_i u_ij (j > i)
 __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda, int64_t M, const double *U, int nb) {
     extern __shared__ double tsm[];  // u_ij at tsm[j * LDD + i], j < 2 * NBD (zero past nb)
+    __shared__ double rinv[NBD];     // 1 / u_ii: tensor mode multiplies (a division is 126 cycles of chain)
 #pragma unroll 16
     for (int e = threadIdx.x; e < 2 * NBD * NBD; e += blockDim.x) {
         const int i = e & (NBD - 1), j = e >> 6;
         tsm[j * LDD + i] = (i < nb && j < nb) ? U[i + (int64_t)j * lda] : (i == j && j < NBD ? 1.0 : 0.0);
     }
+    if (threadIdx.x < NBD)
+        rinv[threadIdx.x] = threadIdx.x < nb ? 1.0 / U[threadIdx.x + (int64_t)threadIdx.x * lda] : 1.0;
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= M) return;
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda,
 #pragma unroll 1
     for (int i = 0; i < nb; ++i) {
         const double *ui = tsm + i;  // u_{i, i + j} at ui[(i + j) * LDD]
-        const double x = sv[0] / ui[i * LDD];
+        const double x = sv[0] * rinv[i];
         row[i * lda] = x;
 #pragma unroll
         for (int j = 1; j < NBD; ++j) sv[j - 1] = fma(-x, ui[(i + j) * LDD], sv[j]);
