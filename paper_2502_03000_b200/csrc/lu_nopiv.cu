@@ -222,7 +222,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     // LM_NOPIV_TRACE=1: per-phase device time on each stream (stderr)
     static const bool trace = getenv("LM_NOPIV_TRACE") != nullptr;
     std::vector<cudaEvent_t> evs;
-    std::vector<int> tags;  // hi: 0 diag, 1 trsm_ru, 2 trsm_ll, 3 gemm, 4 wait for lo; 5 lo
+    std::vector<int> tags;  // hi: 0 diag, 1 trsm_ru, 2 trsm_ll, 3 gemm, 4 wait for lo; lo: 6 wait, 7 U12, 8 update
     auto mark = [&](cudaStream_t str, int tag) {
         if (!trace) return;
         cudaEvent_t e;
@@ -282,19 +282,19 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         // the rank-nob update of the rows below
         auto u12 = [&](int64_t c0, int64_t nc, cudaStream_t str, bool hi) -> int {
             if (int rc = trsm_ll(A + J0 + c0 * lda, nc, Aaa, na, str)) return rc;
-            if (hi) mark(str, 2);
+            mark(str, hi ? 2 : 7);
             if (nbb > 0) {
                 if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + c0 * lda, lda, A + Ja + c0 * lda, lda, nbb, nc,
                                        na, str))
                     return rc;
-                if (hi) mark(str, 3);
+                mark(str, hi ? 3 : 7);
                 if (int rc = trsm_ll(A + Ja + c0 * lda, nc, Abb, nbb, str)) return rc;
-                if (hi) mark(str, 2);
+                mark(str, hi ? 2 : 7);
             }
             if (int rc = dgemm_sub(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1, nc,
                                    nob, str))
                 return rc;
-            if (hi) mark(str, 3);
+            mark(str, hi ? 3 : 8);
             return 0;
         };
         // the remaining columns on the low-priority stream (after the previous
@@ -302,8 +302,8 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         const int64_t nn2 = n - J2;
         if (nn2 > 0) {
             LM_CUDA(cudaStreamWaitEvent(st.lo, ev_l21, 0));
+            mark(st.lo, 6);
             if (int rc = u12(J2, nn2, st.lo, false)) return rc;
-            mark(st.lo, 5);
         }
         // the next outer panel's columns were last written by the previous
         // block's trailing update: wait for it, then their U12 and update
@@ -317,18 +317,19 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         const double host_us =
             std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count();
         cudaDeviceSynchronize();
-        double tot[6] = {0, 0, 0, 0, 0, 0}, last_hi = 0, last_lo = 0;
+        double tot[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, last_hi = 0, last_lo = 0;
         float t;
         for (size_t i = 2; i < evs.size(); ++i) {
-            const bool lo = tags[i] == 5;
+            const bool lo = tags[i] >= 5;
             cudaEventElapsedTime(&t, evs[0], evs[i]);
             double &last = lo ? last_lo : last_hi;
             tot[tags[i]] += t - last;
             last = t;
         }
         fprintf(stderr, "NOPIVTRACE host issue %.0f us | hi: diag %.2f ms, trsm_ru %.2f, trsm_ll %.2f, gemm %.2f, "
-                        "wait for lo %.2f, end %.2f ms | lo: end %.2f ms\n",
-                host_us, tot[0], tot[1], tot[2], tot[3], tot[4], last_hi, last_lo);
+                        "wait for lo %.2f, end %.2f ms | lo: wait for hi %.2f, U12 solves + small gemm %.2f, "
+                        "trailing gemm %.2f, end %.2f ms\n",
+                host_us, tot[0], tot[1], tot[2], tot[3], tot[4], last_hi, tot[6], tot[7], tot[8], last_lo);
         for (auto e : evs) cudaEventDestroy(e);
     }
     if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
