@@ -32,7 +32,12 @@ namespace lm {
 namespace {
 
 constexpr int KC = 16;      // k rows per stage
-constexpr int LDK = KC + 4; // smem row length (elements) of the K-contiguous tiles
+// smem row length (elements) of the K-contiguous tiles: 16-byte rows, as
+// short as that allows (f64 n = 64: 4 instead of 3 CTAs per SM, 2.83 ->
+// 2.65 ms on config 5a's class; n = 32 measured slightly faster with
+// KC + 4); the half kernel keeps KC + 4
+template <class T, int N> constexpr int LDKT = (sizeof(T) == 8 && N == 64) ? KC + 2 : KC + 4;
+constexpr int LDKH = KC + 4;
 
 __device__ __forceinline__ void cpa16(void *smem, const void *gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -48,6 +53,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 template <class T, int N> struct Smem {
+    static constexpr int LDK = LDKT<T, N>;
     static constexpr int LDI = N + 16 / (int)sizeof(T);  // column-chunk row length (keeps 16 B alignment)
     T a[2][N * LDK];   // A(k, m), k in chunk: [m][k]
     T b[2][N * LDK];   // B(k, n), k in chunk: [n][k]
@@ -58,6 +64,7 @@ template <class T, int N> struct Smem {
 // Stage chunk c of instance (pa, pb) into buffer `buf`.
 template <class T, int N>
 __device__ __forceinline__ void stage(Smem<T, N> &sm, int buf, const T *pa, const T *pb, int c) {
+    constexpr int LDK = LDKT<T, N>;
     constexpr int V = 16 / sizeof(T);  // elements per 16-byte copy
     const int k0 = c * KC;
     constexpr int ROWV = KC / V;        // 16-byte pieces per column of a row-chunk
@@ -83,6 +90,7 @@ __global__ void __launch_bounds__(2 * N) atb_schur_trace_tc(int64_t batch, const
     constexpr int NT = 2 * N;
     constexpr int NCH = N / KC;
     constexpr int LDI = Smem<T, N>::LDI;
+    constexpr int LDK = LDKT<T, N>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nn = (int64_t)N * N;
 
@@ -260,8 +268,8 @@ __global__ void __launch_bounds__(2 * N) atb_schur_trace_tc(int64_t batch, const
 constexpr int HN = 128, HH = 64;
 template <class T> struct SmemHalf {
     static constexpr int LDI = HH + 16 / (int)sizeof(T);
-    T a[2][HN * LDK];   // A(k, m), all m: [m][k]
-    T b[2][HH * LDK];   // B(k, n), n in this half: [n][k]
+    T a[2][HN * LDKH];   // A(k, m), all m: [m][k]
+    T b[2][HH * LDKH];   // B(k, n), n in this half: [n][k]
     T ac[2][KC * LDI];  // A(i, k), i in this half: [k][i]
     T red[32];
     T peer;             // the other CTA's trace partial
@@ -274,11 +282,11 @@ __device__ __forceinline__ void stage_half(SmemHalf<T> &sm, int buf, const T *pa
     constexpr int ROWV = KC / V;
     for (int e = threadIdx.x; e < HN * ROWV; e += 256) {
         const int col = e / ROWV, piece = e % ROWV;
-        cpa16(&sm.a[buf][col * LDK + piece * V], pa + (int64_t)col * HN + k0 + piece * V);
+        cpa16(&sm.a[buf][col * LDKH + piece * V], pa + (int64_t)col * HN + k0 + piece * V);
     }
     for (int e = threadIdx.x; e < HH * ROWV; e += 256) {
         const int col = e / ROWV, piece = e % ROWV;
-        cpa16(&sm.b[buf][col * LDK + piece * V], pb + (int64_t)(h * HH + col) * HN + k0 + piece * V);
+        cpa16(&sm.b[buf][col * LDKH + piece * V], pb + (int64_t)(h * HH + col) * HN + k0 + piece * V);
     }
     constexpr int COLV = HH / V;
     for (int e = threadIdx.x; e < KC * COLV; e += 256) {
@@ -338,9 +346,9 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_half(int64_t batch, co
                 for (int kk = 0; kk < KC; kk += 4) {
                     double af[4], bf[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * LDK + kk + fc];
+                    for (int i = 0; i < 4; ++i) af[i] = as[(wm + i * 8 + fr) * LDKH + kk + fc];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) bf[j] = bs[(wn + j * 8 + fr) * LDK + kk + fc];
+                    for (int j = 0; j < 4; ++j) bf[j] = bs[(wn + j * 8 + fr) * LDKH + kk + fc];
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -352,9 +360,9 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_half(int64_t batch, co
                 for (int kl = 0; kl < KC; ++kl) {
                     float av[8], bv[4];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) av[i] = as[(trw + 16 * i) * LDK + kl];
+                    for (int i = 0; i < 8; ++i) av[i] = as[(trw + 16 * i) * LDKH + kl];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) bv[j] = bs[(tcl + 16 * j) * LDK + kl];
+                    for (int j = 0; j < 4; ++j) bv[j] = bs[(tcl + 16 * j) * LDKH + kl];
 #pragma unroll
                     for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -368,7 +376,7 @@ __global__ void __launch_bounds__(256, 2) atb_schur_trace_half(int64_t batch, co
 #pragma unroll
                 for (int q = 0; q < KC / 4; ++q) {
                     const int kl = quarter * (KC / 4) + q;
-                    tr = fma(ac[kl * LDI + i], bs[i * LDK + kl], tr);
+                    tr = fma(ac[kl * LDI + i], bs[i * LDKH + kl], tr);
                 }
             }
             __syncthreads();
