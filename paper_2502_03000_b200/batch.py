@@ -128,7 +128,8 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
     if n != n2 or b.shape[1] != n or b.shape[2] != 1:
         raise KernelContractError("solve_batched: A must be (batch, n, n) and b (batch, n, 1)")
     x = torch.empty((bt, 1, n), dtype=A.dtype, device=A.device).transpose(1, 2)
-    if b.stride() == x.stride() and b.storage_offset() == 0 and b.untyped_storage().nbytes() == x.numel() * 8:
+    if (b.dtype == x.dtype and b.stride() == x.stride() and b.storage_offset() == 0
+            and b.untyped_storage().nbytes() == x.numel() * x.element_size()):
         x.untyped_storage().copy_(b.untyped_storage(), non_blocking=True)  # one DMA copy, no kernel
     else:
         x.copy_(b)
