@@ -689,44 +689,38 @@ __global__ void __launch_bounds__(64, 6)
         }
         return;
     }
-    // back sweep (lazymat/_loops.py:254-258), blocked: thread t owns
-    // position t; per block of 8 positions (descending) the owning warp
-    // finishes the block with shuffles (x_j = c_j / U[j,j], then the
-    // block's positions above j), then every position above the block
-    // applies the block's 8 updates, j descending -- each c_i still sees
-    // j = n-1, n-2, ..., i+1 in the reference's order.
+    // back sweep (lazymat/_loops.py:254-258) by warp 0 alone, no block
+    // barrier: lane l holds positions l and l + 32; per step j (descending)
+    // the owner divides (certified quotient, reciprocal of U[j,j] from (a)),
+    // one shuffle hands x_j to the warp, every position above j subtracts
+    // U[i,j] x_j -- each c_i sees j = n-1, ..., i+1 in the reference's order.
     LU4B_MARK(25)
-    const CertDiv dd = cdiv_prep(t < n ? f.Us[upacked_off(t)] : 1.0, t < n ? f.yd[t] : 1.0);
-    double ci = t < n ? f.xs[t] : 0.0;
-    const int offt = upacked_off(t) - t;  // U[t, j] at offt + j
+    double c0v = 0.0, c1v = 0.0;
+    if (w == 0) {
+        const int i0 = lane, i1 = lane + 32;
+        const CertDiv d0 = cdiv_prep(i0 < n ? f.Us[upacked_off(i0)] : 1.0, i0 < n ? f.yd[i0] : 1.0);
+        const CertDiv d1 = cdiv_prep(i1 < n ? f.Us[upacked_off(i1)] : 1.0, i1 < n ? f.yd[i1] : 1.0);
+        const int off0 = upacked_off(i0) - i0, off1 = upacked_off(i1) - i1;  // U[i, j] at off + j
+        c0v = i0 < n ? f.xs[i0] : 0.0;
+        c1v = i1 < n ? f.xs[i1] : 0.0;
 #pragma unroll 1
-    for (int kb = NB - 1; kb >= 0; --kb) {
-        const int c0 = kb * KB;
-        if (c0 >= n) continue;
-        const int top = min(KB, (int)n - c0);  // real positions in this block
-        if (w == (c0 >> 5)) {
-            const int ls = t - c0;
-#pragma unroll
-            for (int s = KB - 1; s >= 0; --s) {
-                if (s < top) {  // warp-uniform
-                    const int j = c0 + s;
-                    // branch-free: every lane divides by its own diagonal
-                    // (only the owner's quotient and certificate are used)
-                    int bq = 0;
-                    const double q = cdiv(ci, dd, bq);
-                    bad |= (ls == s) & bq;
-                    const double xj = __shfl_sync(MASK, q, j & 31);
-                    const double upd = __dsub_rn(ci, __dmul_rn(f.Us[offt + j], xj));
-                    ci = ls == s ? xj : ((unsigned)ls < (unsigned)s ? upd : ci);
-                }
-            }
-            if (ls >= 0 && ls < KB) f.xs[t] = ci;  // x of the block's positions
+        for (int j = (int)n - 1; j >= 32; --j) {  // owner in the upper half
+            int bq = 0;
+            const double q = cdiv(c1v, d1, bq);
+            bad |= (i1 == j) & bq;
+            const double xj = __shfl_sync(MASK, q, j - 32);
+            const double up1 = __dsub_rn(c1v, __dmul_rn(f.Us[off1 + j], xj));
+            c1v = i1 == j ? xj : (i1 < j ? up1 : c1v);
+            c0v = __dsub_rn(c0v, __dmul_rn(f.Us[off0 + j], xj));  // every lower position is above j
         }
-        __syncthreads();
-        if (t < c0) {
-#pragma unroll
-            for (int s = KB - 1; s >= 0; --s)
-                if (s < top) ci = __dsub_rn(ci, __dmul_rn(f.Us[offt + c0 + s], f.xs[c0 + s]));
+#pragma unroll 1
+        for (int j = min((int)n, 32) - 1; j >= 0; --j) {
+            int bq = 0;
+            const double q = cdiv(c0v, d0, bq);
+            bad |= (i0 == j) & bq;
+            const double xj = __shfl_sync(MASK, q, j);
+            const double up0 = __dsub_rn(c0v, __dmul_rn(f.Us[off0 + j], xj));
+            c0v = i0 == j ? xj : (i0 < j ? up0 : c0v);
         }
     }
     if (__syncthreads_or(bad)) {  // an uncertified quotient: the pivoting kernel redoes the system
@@ -737,9 +731,14 @@ __global__ void __launch_bounds__(64, 6)
         return;
     }
     LU4B_MARK(26)
-    if (t == 0) info[b] = 0;
-    if (piv && t < n) piv[b * n + t] = t;
-    if (t < n) X[b * n + t] = ci;
+    if (w != 0) return;
+    if (lane == 0) info[b] = 0;
+    if (piv) {
+        if (lane < n) piv[b * n + lane] = lane;
+        if (lane + 32 < n) piv[b * n + lane + 32] = lane + 32;
+    }
+    if (lane < n) X[b * n + lane] = c0v;
+    if (lane + 32 < n) X[b * n + lane + 32] = c1v;
 }
 #undef LU4B_MARK
 
