@@ -652,12 +652,10 @@ __global__ void __launch_bounds__(64, 6)
         if (TRACE && lane == 0 && kb < 4) trace[b * 64 + w * 32 + 27 + kb] = clock64();  // (c) done
         // (b) the rows below: divide and eliminate the own panel values
         if (t >= c0 + KB) {
-            CertDiv dv[KB];
-#pragma unroll
-            for (int s = 0; s < KB; ++s) dv[s] = cdiv_prep(f.U11[s][s], f.yd[c0 + s]);
 #pragma unroll
             for (int s = 0; s < KB; ++s) {
-                const double m = cdiv(r[c0 + s], dv[s], bad);
+                const CertDiv dv = cdiv_prep(f.U11[s][s], f.yd[c0 + s]);
+                const double m = cdiv(r[c0 + s], dv, bad);
                 bad |= !(fabs(m) < 1.0);
                 f.Lr[s][t] = m;
 #pragma unroll
