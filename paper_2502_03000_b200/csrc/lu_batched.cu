@@ -598,11 +598,17 @@ __global__ void __launch_bounds__(64, 6)
             const bool diag = (unsigned)ls < (unsigned)KB;
 #pragma unroll
             for (int s = 0; s < KB; ++s) {
-                const int src = (c0 + s) & 31;
-                const double pv = __shfl_sync(MASK, r[c0 + s], src);
+                // the pivot row of step c0+s is final: its owner publishes it
+                // (U11 row s) and the warp reads it back as broadcasts
+                if (ls == s) {
+#pragma unroll
+                    for (int s2 = s; s2 < KB; ++s2) f.U11[s][s2] = r[c0 + s2];
+                }
+                __syncwarp();
+                const double pv = f.U11[s][s];
                 double u[KB];
 #pragma unroll
-                for (int s2 = s + 1; s2 < KB; ++s2) u[s2] = __shfl_sync(MASK, r[c0 + s2], src);
+                for (int s2 = s + 1; s2 < KB; ++s2) u[s2] = f.U11[s][s2];
                 // branch-free: every lane divides, only the block's rows
                 // below the pivot keep the result
                 const bool act = diag && ls > s;
@@ -621,9 +627,6 @@ __global__ void __launch_bounds__(64, 6)
                 for (int s2 = 1; s2 < KB; ++s2)
                     if (ls == s2) ukk = r[c0 + s2];
                 f.yd[c0 + ls] = __drcp_rn(ukk);  // U[k,k] is final: its reciprocal for (b) and the back sweep
-                double2 *u11 = reinterpret_cast<double2 *>(f.U11[ls]);
-#pragma unroll
-                for (int i = 0; i < KB / 2; ++i) u11[i] = make_double2(r[c0 + 2 * i], r[c0 + 2 * i + 1]);
 #pragma unroll
                 for (int s2 = 0; s2 < KB; ++s2)
                     if (s2 >= ls) f.Us[upacked_off(c0 + ls) + s2 - ls] = r[c0 + s2];
