@@ -128,9 +128,9 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
     if n != n2 or b.shape[1] != n or b.shape[2] != 1:
         raise KernelContractError("solve_batched: A must be (batch, n, n) and b (batch, n, 1)")
     x = torch.empty((bt, 1, n), dtype=A.dtype, device=A.device).transpose(1, 2)
-    if (b.dtype == x.dtype and b.stride() == x.stride() and b.storage_offset() == 0
-            and b.untyped_storage().nbytes() == x.numel() * x.element_size()):
-        x.untyped_storage().copy_(b.untyped_storage(), non_blocking=True)  # one DMA copy, no kernel
+    if b.dtype == x.dtype and b.stride() == x.stride():
+        # both dense with the same layout: one flat copy (cudaMemcpyAsync)
+        x.as_strided((x.numel(),), (1,)).copy_(b.as_strided((b.numel(),), (1,), b.storage_offset()))
     else:
         x.copy_(b)
     if n <= 64 and A.dtype == torch.float64:
@@ -143,7 +143,10 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
         host_t.copy_(ci, non_blocking=True)
         torch.cuda.current_stream(A.device).synchronize()
         host = host_t.numpy()
-        cls, hinfo = host[:bt].astype(np.int8), host[bt:].copy()
+        cls, hinfo = host[:bt], host[bt:]
+        if not cls.any() and not hinfo.any():  # every instance general and solved (the common case)
+            return BatchSolveResult(x, np.zeros(bt, dtype=np.int8))
+        cls, hinfo = cls.astype(np.int8), hinfo.copy()
     else:
         info = analyze_batched(A)
         band, triu, tril, symm = _classify(info, n)
