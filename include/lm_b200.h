@@ -182,6 +182,12 @@ int lm_lu_solve_batched(int dtype, int64_t n, int64_t batch, const void *a, void
  * 32 < n <= 64, as above), one host read. */
 int lm_solve_batched_classified(int dtype, int64_t n, int64_t batch, const void *a, void *x, int32_t *d_cls,
                                 int32_t *d_info, void *stream);
+/* lm_solve_batched_classified with the right-hand sides read from b (dense,
+ * batch*n contiguous doubles) and the solutions written to x (same layout;
+ * b == x is the in-place call): the copy is one cudaMemcpyAsync on `stream`
+ * inside the call instead of a separate framework copy. */
+int lm_solve_batched_classified_from(int dtype, int64_t n, int64_t batch, const void *a, const void *b, void *x,
+                                     int32_t *d_cls, int32_t *d_info, void *stream);
 /* Batched structure classification of `batch` contiguous F-order n x n
  * matrices: d_out[3*b + {0,1,2}] = lbw, ubw, sym. */
 int lm_analyze_batched(int dtype, int64_t n, int64_t batch, const void *a, int64_t *d_out, void *stream);

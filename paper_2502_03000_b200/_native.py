@@ -34,7 +34,7 @@ EXPORTS = (
     "lm_diag_scale", "lm_diag_of_product", "lm_trace_of_product", "lm_triple_diag_dot",
     "lm_analyze", "lm_lu_factor", "lm_lu_factor_mode", "lm_lu_solve", "lm_band_solve", "lm_tri_solve",
     "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
-    "lm_lu_solve_batched", "lm_solve_batched_classified", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
+    "lm_lu_solve_batched", "lm_solve_batched_classified", "lm_solve_batched_classified_from", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
     "lm_fill_pcg64", "lm_nccl_load", "lm_nccl_unique_id", "lm_nccl_init_rank", "lm_nccl_init_all",
     "lm_allreduce_sum", "lm_allreduce_sum_f64", "lm_nccl_destroy",
     "lm_debug_lu_panel",
@@ -80,6 +80,7 @@ _SIGS = {
     "lm_set_identity": (_i, [_i, View, _p]),
     "lm_lu_solve_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p]),
     "lm_solve_batched_classified": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p]),
+    "lm_solve_batched_classified_from": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p]),
     "lm_analyze_batched": (_i, [_i, _i64, _i64, _p, _p, _p]),
     "lm_expr_atb_schur_trace_batched": (_i, [_i, _i64, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "lm_fill_uniform": (_i, [_i, View, ctypes.c_uint64, _i64, _i64, _i64, _d, _d, _p]),

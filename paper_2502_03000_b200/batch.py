@@ -128,17 +128,18 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
     if n != n2 or b.shape[1] != n or b.shape[2] != 1:
         raise KernelContractError("solve_batched: A must be (batch, n, n) and b (batch, n, 1)")
     x = torch.empty((bt, 1, n), dtype=A.dtype, device=A.device).transpose(1, 2)
-    if b.dtype == x.dtype and b.stride() == x.stride():
-        # both dense with the same layout: one flat copy (cudaMemcpyAsync)
-        x.as_strided((x.numel(),), (1,)).copy_(b.as_strided((b.numel(),), (1,), b.storage_offset()))
-    else:
-        x.copy_(b)
+    # b dense (batch*n consecutive elements, as _check_batch guarantees) and of x's type
+    same = b.dtype == x.dtype and b.stride(0) == n and (n == 1 or b.stride(1) == 1)
     if n <= 64 and A.dtype == torch.float64:
         # one kernel: structure class + exact LU solve of every instance; one
-        # host read of (class, info) into pinned memory
+        # host read of (class, info) into pinned memory; b is copied into x
+        # inside the call (one cudaMemcpyAsync)
+        if not same:
+            x.copy_(b)
+        src = b if same else x
         ci = torch.empty(2 * bt, dtype=torch.int32, device=A.device)
-        N.call("lm_solve_batched_classified", N.dtype_code(A), n, bt, A.data_ptr(), x.data_ptr(), ci.data_ptr(),
-               ci.data_ptr() + 4 * bt)
+        N.call("lm_solve_batched_classified_from", N.dtype_code(A), n, bt, A.data_ptr(), src.data_ptr(),
+               x.data_ptr(), ci.data_ptr(), ci.data_ptr() + 4 * bt)
         host_t = _pinned_i32(2 * bt)
         host_t.copy_(ci, non_blocking=True)
         torch.cuda.current_stream(A.device).synchronize()
@@ -148,6 +149,10 @@ def solve_batched(A: torch.Tensor, b: torch.Tensor, *, check: bool = True) -> Ba
             return BatchSolveResult(x, np.zeros(bt, dtype=np.int8))
         cls, hinfo = cls.astype(np.int8), hinfo.copy()
     else:
+        if same:
+            x.as_strided((x.numel(),), (1,)).copy_(b.as_strided((b.numel(),), (1,), b.storage_offset()))
+        else:
+            x.copy_(b)
         info = analyze_batched(A)
         band, triu, tril, symm = _classify(info, n)
         cls = np.zeros(bt, dtype=np.int8)

@@ -1051,3 +1051,17 @@ extern "C" int lm_solve_batched_classified(int dtype, int64_t n, int64_t batch, 
     return launch_batched<true>(n, batch, (const double *)a, (double *)x, nullptr, nullptr, d_info, d_cls,
                                 as_stream(stream));
 }
+
+extern "C" int lm_solve_batched_classified_from(int dtype, int64_t n, int64_t batch, const void *a, const void *b,
+                                                void *x, int32_t *d_cls, int32_t *d_info, void *stream) {
+    clear_error();
+    LM_REQUIRE(dtype == LM_F64, "solve_batched_classified_from: f64 only");
+    LM_REQUIRE(n >= 1 && n <= 64, "solve_batched_classified_from: 1 <= n <= 64 (got %lld)", (long long)n);
+    if (batch == 0) return 0;
+    LM_REQUIRE(batch <= 0x7fffffff, "solve_batched_classified_from: batch too large");
+    if (b != x)
+        LM_CUDA(cudaMemcpyAsync(x, b, sizeof(double) * (size_t)(n * batch), cudaMemcpyDeviceToDevice,
+                                as_stream(stream)));
+    return launch_batched<true>(n, batch, (const double *)a, (double *)x, nullptr, nullptr, d_info, d_cls,
+                                as_stream(stream));
+}
