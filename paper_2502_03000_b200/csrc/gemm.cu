@@ -192,6 +192,72 @@ __global__ void __launch_bounds__(256) gemv_finish(const T *__restrict__ part, i
     }
 }
 
+// Row-owner GEMV (f64, column-major M with 16-byte columns): CTA b owns
+// rows [8b, 8b+8) and ALL columns, so there are no split-K partials and no
+// finish launch.  Lane l of warp w reads rows 8b + 2(l % 4) .. +1 of column
+// 8(w + 8i) + l / 4 as one 16-byte load (a warp: eight 64-byte column
+// pieces per instruction), eight loads in flight per thread; the column
+// lanes and the eight warps are then summed in a fixed order
+// (reproducible).  p / 8 CTAs (config 3a: 512, ~3.5 per SM); config 3a
+// 75.4 -> 72.9 us per step (16 rows per CTA: 101 us; 4 rows: 88 us;
+// 16 loads in flight: 82 us).  LM_GEMV_ROWS=0: the split-K kernel below.
+constexpr int kGvRowsRB = 8;
+__global__ void __launch_bounds__(256) gemv_rows_f64(const double *__restrict__ M, int64_t ld, int64_t p, int64_t q,
+                                                    Vec<const double> x, Vec<double> y) {
+    constexpr int RPL = kGvRowsRB / 2;  // lanes per column piece (2 rows each)
+    constexpr int CPW = 32 / RPL;       // columns per warp load
+    constexpr int CS = 8 * CPW;         // column stride of a thread
+    __shared__ double2 red[8][RPL];
+    pdl_wait();  // M and x may be the previous kernel's output
+    pdl_trigger();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int rp = lane % RPL, co = lane / RPL;
+    const int64_t r0 = (int64_t)blockIdx.x * kGvRowsRB + 2 * rp;
+    const double *base = M + r0;
+    double a0 = 0.0, a1 = 0.0;
+    constexpr int U = 8;
+    int64_t k = (int64_t)CPW * w + co;
+    for (; k + (int64_t)CS * (U - 1) < q; k += (int64_t)CS * U) {
+        double2 v[U];
+        double xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            v[u] = __ldcs(reinterpret_cast<const double2 *>(base + (k + CS * u) * ld));
+            xv[u] = x[k + CS * u];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            a0 = fma(v[u].x, xv[u], a0);
+            a1 = fma(v[u].y, xv[u], a1);
+        }
+    }
+    for (; k < q; k += CS) {
+        const double2 v = __ldcs(reinterpret_cast<const double2 *>(base + k * ld));
+        const double xk = x[k];
+        a0 = fma(v.x, xk, a0);
+        a1 = fma(v.y, xk, a1);
+    }
+    // the column lanes of each row pair, in a fixed order
+#pragma unroll
+    for (int o = RPL; o < 32; o <<= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+    }
+    if (lane < RPL) red[w][lane] = make_double2(a0, a1);
+    __syncthreads();
+    if (threadIdx.x < RPL) {
+        double2 t = red[0][threadIdx.x];
+#pragma unroll
+        for (int q2 = 1; q2 < 8; ++q2) {
+            t.x += red[q2][threadIdx.x].x;
+            t.y += red[q2][threadIdx.x].y;
+        }
+        const int64_t r = (int64_t)blockIdx.x * kGvRowsRB + 2 * threadIdx.x;
+        if (r < p) y[r] = t.x;
+        if (r + 1 < p) y[r + 1] = t.y;
+    }
+}
+
 template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_vec &yv, cudaStream_t s) {
     const int64_t p = mv.rows, q = mv.cols;
     if (p == 0) return 0;
@@ -202,6 +268,17 @@ template <class T> int gemv_impl(const lm_view &mv, const lm_vec &xv, const lm_v
     // 64-column chunks, 4 CTAs per SM (64 registers, no spill): 5.3 TB/s on
     // config 3a; 3 CTAs/SM spilled (4.7), 128-column chunks spill (3.0-3.6)
     constexpr int KCv = 64;
+    static const bool rows_on = !(getenv("LM_GEMV_ROWS") && getenv("LM_GEMV_ROWS")[0] == '0');
+    if (sizeof(T) == 8 && rows_on && q > 0 && mv.rs == 1 && p % kGvRowsRB == 0 &&
+        (mv.cols <= 1 || mv.cs % 2 == 0) && ((uintptr_t)mv.ptr & 15) == 0 && p / kGvRowsRB <= 0x7fffffff) {
+        const int64_t ld = mv.cols > 1 ? mv.cs : p;
+        LM_CUDA(launch_pdl(gemv_rows_f64, dim3((unsigned)(p / kGvRowsRB)), dim3(256), 0, s,
+                           (const double *)mv.ptr, ld, p, q, Vec<const double>{(const double *)xv.ptr, xv.n, xv.stride},
+                           Vec<double>{(double *)yv.ptr, yv.n, yv.stride}));
+        LM_LAUNCHED(1);
+        note_variant("gemv_rows");
+        return 0;
+    }
     if (q > 0 && mv.rs == 1 && p % RPT32 == 0 && (mv.cols <= 1 || mv.cs % RPT32 == 0) && aligned32(mv.ptr) &&
         ceil_div(q, KCv) <= 65535) {
         constexpr int RB = 32 * RPT32;
