@@ -513,3 +513,24 @@ def test_chain_plan_fused_with_identical_events(monkeypatch):
     assert kinds.count("kernel") == 2 and [e.name for e in tr.events if e.kind == "kernel"] == ["gemm", "gemm"]
     ref = X.to_numpy() @ (Y.to_numpy() @ Z.to_numpy())
     assert normwise(tr.result.to_numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("pq,off", [((4096, 4096), 0), ((1024, 1000), 2), ((8, 3), 0), ((520, 65), 4),
+                                    ((2048, 1), 0), ((1000, 333), 0)])
+def test_gemv_row_owner_path_views(pq, off):
+    """Column-major f64 GEMV on the row-owner kernel (no split-K finish):
+    plain matrices and column-major sub-views whose leading dimension
+    exceeds their row count (rows [off, off+p) of a taller matrix, 16-byte
+    aligned when off is even), ragged column counts, a single column."""
+    p, q = pq
+    rng = np.random.default_rng(p * 11 + q + off)
+    big = np.asfortranarray(rng.uniform(-1, 1, (p + 2 * off + 6, q)))
+    a = big[off:off + p, :]
+    x = rng.uniform(-1, 1, q)
+    ref = np.zeros(p)
+    O.gemv(np.asfortranarray(a), x, ref, False)
+    dbig = dev(big)
+    da = dbig[off:off + p, :]
+    out = torch.empty(p, dtype=torch.float64, device=DEV)
+    K.gemv(da, torch.from_numpy(x).to(DEV), out, False)
+    assert normwise(host(out), ref) <= 1e-12
