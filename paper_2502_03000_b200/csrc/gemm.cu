@@ -999,6 +999,10 @@ int dgemm_cfg(GemmArgs &g, bool a_cm, bool b_cn, bool va, bool vb, cudaStream_t 
     return 0;
 }
 
+// gemm_skinny.cu: one or two short dimensions (0 launched, 1 not taken, < 0 error)
+int try_dgemm_skinny(const double *a, int64_t a_sm, int64_t a_sk, const double *b, int64_t b_sk, int64_t b_sn,
+                     double *c, int64_t c_sm, int64_t c_sn, int64_t M, int64_t N, int64_t K, cudaStream_t s);
+
 // A(m,k) strides (a_sm, a_sk), B(k,n) strides (b_sk, b_sn).
 int dgemm(const double *a, int64_t a_sm, int64_t a_sk, const double *b, int64_t b_sk, int64_t b_sn, double *c,
           int64_t c_sm, int64_t c_sn, int64_t M, int64_t N, int64_t K, bool syrk, cudaStream_t s) {
@@ -1008,6 +1012,10 @@ int dgemm(const double *a, int64_t a_sm, int64_t a_sk, const double *b, int64_t 
         LM_REQUIRE(c_sm == 1, "gemm: K == 0 needs a column-major output");
         for (int64_t n = 0; n < N; ++n) LM_CUDA(cudaMemsetAsync(c + n * c_sn, 0, sizeof(double) * M, s));
         return 0;
+    }
+    if (!syrk) {
+        const int rc = try_dgemm_skinny(a, a_sm, a_sk, b, b_sk, b_sn, c, c_sm, c_sn, M, N, K, s);
+        if (rc <= 0) return rc;
     }
     GemmArgs g{};
     g.a = a;
