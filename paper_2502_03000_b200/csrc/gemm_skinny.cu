@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(SKT, 1) dgemm_tallk(SkinnyArgs g) {
     if (direct) return;
     stamp(g, 2);
     cg::this_grid().sync();
+    pdl_trigger();  // the next kernel's launch may be processed while the slices are summed
     stamp(g, 3);
     // C slice = sum of the partials in a fixed order: thread (zg, el) sums the
     // partials z = zg (mod ZG) of element el of the pass, the ZG group sums are

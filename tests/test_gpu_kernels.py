@@ -200,6 +200,49 @@ def test_gemm_normwise(pqr, layout):
     assert normwise(host(out), ref) <= 1e-12
 
 
+# (M, K, N, lda pad, ldb pad, expected kernel): the skinny kernels (gemm_skinny.cu)
+# and the shapes just outside them
+SKINNY = [
+    (100, 8000, 100, 0, 0, "gemm_tallk"),      # config 3b's Y * Z: A in 16-row pieces, one partial last group
+    (96, 4096, 40, 0, 0, "gemm_tallk"),        # M = 0 (mod 16): A row by row
+    (128, 9472, 128, 0, 0, "gemm_tallk"),      # the largest tile and K slice (64 per SM)
+    (100, 2052, 17, 4, 6, "gemm_tallk"),       # views: padded leading dimensions, N odd
+    (16, 1024, 16, 0, 0, "gemm_tallk"),        # smallest
+    (128, 9480, 128, 0, 0, "tiled"),           # K slice > 64 per SM: tiled kernel
+    (100, 8001, 100, 0, 0, "tiled"),           # K not a multiple of 4
+    (8000, 100, 100, 0, 0, "gemm_tallm"),      # config 3b's X * T: B in one copy
+    (8000, 100, 100, 2, 4, "gemm_tallm"),      # views: B column by column
+    (1024, 4, 16, 0, 0, "gemm_tallm"),         # smallest: 8-row bands, one K group
+    (20000, 128, 128, 0, 0, "gemm_tallm"),     # largest K and N, several waves of 64-row bands
+    (3002, 72, 33, 0, 0, "gemm_tallm"),        # partial last band, N odd
+    (3001, 72, 33, 0, 0, "tiled"),             # M odd: tiled kernel
+]
+
+
+@pytest.mark.parametrize("case", SKINNY, ids=lambda c: f"{c[0]}x{c[1]}x{c[2]}+{c[3]}+{c[4]}")
+def test_gemm_skinny_kernels(case):
+    """Products with one or two short dimensions against the oracle (1e-12
+    normwise), the kernel that ran asserted, and bit-reproducible run to run
+    (the split-K partials are summed in a fixed order)."""
+    from paper_2502_03000_b200 import _native
+    M, Kd, N, pa, pb, kernel = case
+    rng = np.random.default_rng(M + 3 * Kd + 7 * N)
+    abig = np.asfortranarray(rng.uniform(-1, 1, (M + pa, Kd)))
+    bbig = np.asfortranarray(rng.uniform(-1, 1, (Kd + pb, N)))
+    a, b = abig[:M, :], bbig[:Kd, :]
+    ref = np.zeros((M, N), order="F")
+    O.gemm(np.asfortranarray(a), np.asfortranarray(b), ref)
+    da, db = dev(abig)[:M, :], dev(bbig)[:Kd, :]
+    out = fortran_empty(M, N, device=DEV)
+    K.gemm(da, db, out)
+    ran = _native.last_variant()
+    assert ran == kernel or (kernel == "tiled" and ran in ("gemm_tma", "gemm_cp"))
+    assert normwise(host(out), ref) <= 1e-12
+    again = fortran_empty(M, N, device=DEV)
+    K.gemm(da, db, again)
+    assert torch.equal(out, again)
+
+
 @pytest.mark.parametrize("nk", [(1, 1), (5, 3), (31, 7), (64, 64), (130, 300), (200, 1000)])
 @pytest.mark.parametrize("transposed", [False, True])
 def test_syrk_normwise_and_bitwise_symmetric(nk, transposed):
