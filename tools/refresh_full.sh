@@ -6,7 +6,7 @@ set -u
 O=gpurun_out/prof
 mkdir -p $O
 declare -A K=( [1]="regex:lm_prog" [2]="regex:trace_tiles|diag_scale_cols32" [3a]="regex:gemv_cm32" \
-               [3b]="regex:dgemm_dmma|splitk" [3c]="regex:dgemm_dmma" [4a]="regex:lu_panel_cluster|dgemm_dmma" \
+               [3b]="regex:dgemm_tall|dgemm_dmma|splitk" [3c]="regex:dgemm_dmma" [4a]="regex:lu_panel_cluster|dgemm_dmma" \
                [4b]="regex:lu_batched_nopiv|lu_batched_shift|lu_batched_rows" [5a]="regex:atb_schur" [5a]="regex:atb_schur" [5a-f32]="regex:atb_schur" [5b]="regex:lm_prog|trace_quads" )
 declare -A NC=( [1]=1 [2]=2 [3a]=1 [3b]=2 [3c]=1 [4a]=2 [4b]=2 [5a]=3 [5a-f32]=3 [5b]=2 )
 for C in ${CONFIGS:-2 1 3a 3b 3c 4a 4b 5a 5a-f32 5b}; do
