@@ -145,6 +145,14 @@ int lm_lu_factor_mode(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_info, in
 /* Solve with a factorisation from lm_lu_factor; x (n x m, F-order)
  * arrives holding B and is overwritten with X. */
 int lm_lu_solve(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, void *stream);
+/* lm_lu_solve with the arithmetic chosen like lm_lu_factor_mode's: LM_LU_EXACT
+ * is lm_lu_solve (_lu_solve_inplace's order, lazymat/_loops.py:239-259, bit
+ * for bit); LM_LU_TENSOR (LM_LU_AUTO from n = 2048) runs both substitutions
+ * as FP64 tensor-core products with the diagonal blocks' inverses (scaled
+ * residual <= 1e-10, not bit-identical) when n is a multiple of 64 and the
+ * right-hand sides a multiple of 32, and falls back to the exact order on
+ * the device when a diagonal block is ill-conditioned. */
+int lm_lu_solve_mode(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, int mode, void *stream);
 /* Banded solve (pack + factor + substitute) in place on x; kl/ku are
  * the detected bandwidths.  ab_work: (2kl+ku+1) x n device scratch. */
 int lm_band_solve(int dtype, lm_view a, lm_view x, int64_t kl, int64_t ku, void *ab_work, int64_t *d_piv,

@@ -347,7 +347,9 @@ constexpr int kLuNb = 64;
 
 int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, bool tensor);
 int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s);
-int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s);
+int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s,
+                       const int *only_if);
+int lu_solve_tensor(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s);
 template <bool DESC, bool SKIP_ZERO>
 int exact_update(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc, int64_t M,
                  int64_t N, int K, cudaStream_t s, bool short_ctas = false);
@@ -509,7 +511,7 @@ __global__ void gather_rows(const double *__restrict__ src, int64_t ld_src, cons
 constexpr int kSolveNb = 64;
 
 int lu_solve_impl(const double *LU, int64_t n, int64_t lda, const int64_t *piv, double *X, int64_t ldx, int64_t m,
-                  cudaStream_t s) {
+                  cudaStream_t s, int mode) {
     if (n == 0 || m == 0) return 0;
     // 1. sequential row swaps == one gather by the composed permutation
     Scratch perm, tmp;
@@ -531,8 +533,12 @@ int lu_solve_impl(const double *LU, int64_t n, int64_t lda, const int64_t *piv, 
                               cudaMemcpyDeviceToDevice, s));
     gather_rows<<<(unsigned)ceil_div(n * m, 256), 256, 0, s>>>(tmp.as<double>(), n, perm.as<int32_t>(), n, m, X, ldx);
     LM_LAUNCHED(1);
-    // 2./3. one cooperative wavefront kernel for both sweeps (lu_solve.cu)
-    if (int rc = lu_solve_wavefront(LU, n, lda, X, ldx, m, s); rc != 1) return rc;
+    // 2./3. tensor mode: both sweeps as DMMA products with inverted diagonal
+    // blocks (lu_solve_tc.cu; residual-level, falls back on device)
+    if (lu_tensor_mode(mode, n))
+        if (int rc = lu_solve_tensor(LU, n, lda, X, ldx, m, s); rc != 1) return rc;
+    // exact order: one cooperative wavefront kernel for both sweeps (lu_solve.cu)
+    if (int rc = lu_solve_wavefront(LU, n, lda, X, ldx, m, s, nullptr); rc != 1) return rc;
     // otherwise: forward, unit lower: 32-row block (one thread per rhs
     // column), then the rows below (order-preserving update, k ascending)
     constexpr int SB = 32;
@@ -721,7 +727,18 @@ extern "C" int lm_lu_solve(int dtype, lm_view lu, const int64_t *d_piv, lm_view 
     LM_REQUIRE(lu.rs == 1 && (x.rs == 1 || x.rows <= 1), "lu_solve needs F-order operands");
     const int64_t ldx = x.cols > 1 ? x.cs : (x.rows > 0 ? x.rows : 1);
     return lu_solve_impl((const double *)lu.ptr, lu.rows, lu.cs > 0 ? lu.cs : 1, d_piv, (double *)x.ptr, ldx, x.cols,
-                         as_stream(stream));
+                         as_stream(stream), LM_LU_EXACT);
+}
+
+extern "C" int lm_lu_solve_mode(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, int mode, void *stream) {
+    clear_error();
+    LM_REQUIRE(dtype == LM_F64, "lu_solve: f64 only");
+    LM_REQUIRE(mode == LM_LU_AUTO || mode == LM_LU_EXACT || mode == LM_LU_TENSOR, "lu_solve: bad mode %d", mode);
+    LM_REQUIRE(lu.rows == lu.cols && x.rows == lu.rows, "lu_solve shape mismatch");
+    LM_REQUIRE(lu.rs == 1 && (x.rs == 1 || x.rows <= 1), "lu_solve needs F-order operands");
+    const int64_t ldx = x.cols > 1 ? x.cs : (x.rows > 0 ? x.rows : 1);
+    return lu_solve_impl((const double *)lu.ptr, lu.rows, lu.cs > 0 ? lu.cs : 1, d_piv, (double *)x.ptr, ldx, x.cols,
+                         as_stream(stream), mode);
 }
 
 extern "C" int lm_tri_solve(int dtype, lm_view a, lm_view x, int upper, int32_t *d_info, void *stream) {

@@ -35,6 +35,7 @@ struct WaveArgs {
     int64_t ldx;
     int m, nblk;
     int *flags;  // [2][nblk], zeroed
+    const int *only_if;  // null, or a device flag: do nothing unless it is set (lu_solve_tc.cu's fallback)
 };
 
 __device__ __forceinline__ void wait_flag(const int *f) {
@@ -56,6 +57,7 @@ __device__ __forceinline__ void raise_flag(int *f) {
 }
 
 __global__ void __launch_bounds__(WT, 1) lu_solve_wave(WaveArgs a) {
+    if (a.only_if && *a.only_if == 0) return;  // (uniform over the grid)
     extern __shared__ double sw[];
     double *sL = sw;              // [WB][WLD]: sL[i][j] = T[i0+i, j0+j]
     double *sX = sw + WB * WLD;   // [WB][WLD]: sX[j][c] = X[j0+j, c]
@@ -191,9 +193,11 @@ struct Wave2Args {
     int m, nblk, ngrp;
     int *flags;  // [2][nblk][ngrp], zeroed
     unsigned long long *dbg;  // optional: [2][nblk] globaltimer at each flag raise (group 0)
+    const int *only_if;       // as WaveArgs
 };
 
 __global__ void __launch_bounds__(WT, 2) lu_solve_wave2(Wave2Args a) {
+    if (a.only_if && *a.only_if == 0) return;  // (uniform over the grid)
     extern __shared__ double sw2[];
     double *sL = sw2;              // [WB][WLD]: off-diagonal tile L[i0.., j0..]
     double *sD = sL + WB * WLD;    // [WB][WLD]: this block's diagonal tile (staged once per sweep)
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(WT, 2) lu_solve_wave2(Wave2Args a) {
 }
 
 static int lu_solve_wavefront2(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m,
-                               cudaStream_t s) {
+                               cudaStream_t s, const int *only_if) {
     const int nblk = (int)ceil_div(n, WB), ngrp = (int)ceil_div(m, G2);
     const size_t smem = sizeof(double) * (2 * WB * WLD + 2 * WB * G2LD);
     if (int rc = func_attrs(lu_solve_wave2, smem)) return rc;
@@ -328,7 +332,8 @@ static int lu_solve_wavefront2(const double *LU, int64_t n, int64_t lda, double 
                 return 0;
             }))
             return rc;
-    Wave2Args args{LU, lda, n, X, ldx, (int)m, nblk, ngrp, flags.as<int>(), want && nblk <= 2048 ? dbg : nullptr};
+    Wave2Args args{LU, lda, n, X, ldx, (int)m, nblk, ngrp, flags.as<int>(), want && nblk <= 2048 ? dbg : nullptr,
+                   only_if};
     void *kargs[] = {&args};
     LM_CUDA(cudaLaunchCooperativeKernel((const void *)lu_solve_wave2, dim3(nblk * ngrp), dim3(WT), kargs, smem, s));
     count_launch(1);
@@ -347,10 +352,11 @@ static int lu_solve_wavefront2(const double *LU, int64_t n, int64_t lda, double 
 }
 
 // 0 = done; 1 = not applicable (caller uses the launch-per-block path)
-int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s) {
+int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s,
+                       const int *only_if) {
     if (m < 1 || n < 1) return 1;
     if (m > G2) {  // several right-hand-side groups: independent wavefronts
-        const int rc = lu_solve_wavefront2(LU, n, lda, X, ldx, m, s);
+        const int rc = lu_solve_wavefront2(LU, n, lda, X, ldx, m, s, only_if);
         if (rc != 1) return rc;
     }
     if (m > WM) return 1;
@@ -363,7 +369,7 @@ int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int6
     Scratch flags;
     if (int rc = flags.alloc(sizeof(int) * 2 * nblk, s)) return rc;
     LM_CUDA(cudaMemsetAsync(flags.p, 0, sizeof(int) * 2 * nblk, s));
-    WaveArgs args{LU, lda, n, X, ldx, (int)m, nblk, flags.as<int>()};
+    WaveArgs args{LU, lda, n, X, ldx, (int)m, nblk, flags.as<int>(), only_if};
     void *kargs[] = {&args};
     LM_CUDA(cudaLaunchCooperativeKernel((const void *)lu_solve_wave, dim3(nblk), dim3(WT), kargs, smem, s));
     count_launch(1);

@@ -494,6 +494,54 @@ def test_lu_solve_rhs_groups_bitwise(n, m):
     assert bits_equal(host(x), x_ref)
 
 
+def _scaled_residual(a, x, b):
+    return np.linalg.norm(a @ x - b, np.inf) / (np.linalg.norm(a, np.inf) * np.linalg.norm(x, np.inf) +
+                                                np.linalg.norm(b, np.inf))
+
+
+@pytest.mark.parametrize("kind", ["dominant", "general", "tiny_pivot"])
+def test_lu_solve_tensor_mode(kind):
+    """lm_lu_solve_mode(LM_LU_TENSOR): both substitutions as DMMA products
+    with inverted diagonal blocks (lu_solve_tc.cu).  Dominant matrix: the
+    tensor path runs (bits differ from the exact order, residual <= 1e-10).
+    A diagonal block with a tiny pivot: the device-side guard hands the solve
+    to the exact wavefront, bit-identical to lm_lu_solve.  General matrix:
+    whichever path the guard picks, residual <= 1e-10."""
+    from paper_2502_03000_b200 import _native as N
+    n, k = 2048, 64
+    rng = np.random.default_rng(77)
+    a = rng.uniform(-1, 1, (n, n))
+    if kind == "dominant":
+        a[np.diag_indices(n)] += n
+    elif kind == "tiny_pivot":
+        a = np.triu(a) + 4.0 * np.eye(n)   # upper triangular: no pivoting, U = A
+        a[700, 700] = 1e-7                 # block 10's inverse has entries ~1e7
+    a = np.asfortranarray(a)
+    b = np.asfortranarray(rng.uniform(-1, 1, (n, k)))
+    A = dev(a)
+    lu, piv = K.lu_factor(A, mode="exact")
+    x_exact = dev(b).clone()
+    N.call("lm_lu_solve", 0, N.view(lu.data), piv.data_ptr(), N.view(x_exact))
+    x_tc = dev(b).clone()
+    N.call("lm_lu_solve_mode", 0, N.view(lu.data), piv.data_ptr(), N.view(x_tc), N.LU_MODES["tensor"])
+    assert N.last_variant() == "solve_tc"
+    xe, xt = host(x_exact), host(x_tc)
+    if kind == "tiny_pivot":
+        assert bits_equal(xt, xe)          # guard tripped: the exact kernel solved it
+    else:
+        assert _scaled_residual(a, xt, b) <= 1e-10
+        assert normwise(xt, xe) <= 1e-8
+    if kind == "dominant":
+        assert not bits_equal(xt, xe)      # the tensor path really ran
+        again = dev(b).clone()
+        N.call("lm_lu_solve_mode", 0, N.view(lu.data), piv.data_ptr(), N.view(again), N.LU_MODES["tensor"])
+        assert torch.equal(again, x_tc)    # reproducible run to run
+    # exact mode through the same entry point is lm_lu_solve
+    x_m = dev(b).clone()
+    N.call("lm_lu_solve_mode", 0, N.view(lu.data), piv.data_ptr(), N.view(x_m), N.LU_MODES["exact"])
+    assert torch.equal(x_m, x_exact)
+
+
 @pytest.mark.slow
 def test_config4a_full_size_residual_and_pivots():
     """BASELINE config 4a at full size: A = U(-1,1) + 8192 I, b 8192 x 64."""
