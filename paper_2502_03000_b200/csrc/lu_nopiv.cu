@@ -251,6 +251,9 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         return 0;
     };
     bool rest_pending = false;
+    // opt-in (LM_NOPIV_SPLIT=1): measured slower on config 4a, 28.6 vs 27.9 ms -- the
+    // low-priority stream's GEMM work, not the panel chain's wait, bounds the step
+    static const bool split_rest = getenv("LM_NOPIV_SPLIT") && getenv("LM_NOPIV_SPLIT")[0] == '1';
     for (int64_t J0 = 0; J0 < n; J0 += OB) {
         const int na = (int)((n - J0) < NBD ? (n - J0) : NBD);
         const int64_t Ja = J0 + na;
@@ -291,27 +294,36 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
                 if (int rc = trsm_ll(A + Ja + c0 * lda, nc, Abb, nbb, str)) return rc;
                 mark(str, hi ? 2 : 7);
             }
-            if (int rc = dgemm_sub(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1, nc,
-                                   nob, str))
+            // low-priority stream: the next outer panel's columns first, so the
+            // panel chain (which waits on ev_rest) does not wait for the whole
+            // trailing update
+            const int64_t nfirst = (!hi && split_rest && nc > OB) ? OB : nc;
+            if (int rc = dgemm_sub(A + J1 + J0 * lda, lda, A + J0 + c0 * lda, lda, A + J1 + c0 * lda, lda, n - J1,
+                                   nfirst, nob, str))
                 return rc;
+            if (!hi) LM_CUDA(cudaEventRecord(ev_rest, str));
+            if (nfirst < nc)
+                if (int rc = dgemm_sub(A + J1 + J0 * lda, lda, A + J0 + (c0 + nfirst) * lda, lda,
+                                       A + J1 + (c0 + nfirst) * lda, lda, n - J1, nc - nfirst, nob, str))
+                    return rc;
             mark(str, hi ? 3 : 8);
             return 0;
         };
         // the remaining columns on the low-priority stream (after the previous
         // outer block's, which wrote the same columns)
         const int64_t nn2 = n - J2;
+        // the next outer panel's columns were last written by the first piece
+        // of the previous block's trailing update (ev_rest, recorded inside
+        // u12): the wait is enqueued before this block's update re-records it
+        if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
+        mark(st.hi, 4);
         if (nn2 > 0) {
             LM_CUDA(cudaStreamWaitEvent(st.lo, ev_l21, 0));
             mark(st.lo, 6);
             if (int rc = u12(J2, nn2, st.lo, false)) return rc;
         }
-        // the next outer panel's columns were last written by the previous
-        // block's trailing update: wait for it, then their U12 and update
-        if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
-        mark(st.hi, 4);
         if (int rc = u12(J1, J2 - J1, st.hi, true)) return rc;
         rest_pending = nn2 > 0;
-        if (rest_pending) LM_CUDA(cudaEventRecord(ev_rest, st.lo));
     }
     if (trace) {
         const double host_us =
@@ -332,7 +344,8 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
                 host_us, tot[0], tot[1], tot[2], tot[3], tot[4], last_hi, tot[6], tot[7], tot[8], last_lo);
         for (auto e : evs) cudaEventDestroy(e);
     }
-    if (rest_pending) LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
+    LM_CUDA(cudaEventRecord(ev_rest, st.lo));  // everything on the low-priority stream
+    LM_CUDA(cudaStreamWaitEvent(st.hi, ev_rest, 0));
     LM_CUDA(cudaEventRecord(ev_join, st.hi));
     LM_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     return 0;
