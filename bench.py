@@ -604,9 +604,9 @@ class Config4a(Workload):
 
         def solve():
             x.copy_(b)
-            N.call("lm_lu_solve", 0, N.view(work), piv.data_ptr(), N.view(x))
-        return [("lu_factor (cluster panels + DMMA trailing updates)", 2 * n ** 3 // 3, factor),
-                ("lu_solve (wavefront substitution)", 2 * n * n * k, solve)]
+            N.call("lm_lu_solve_mode", 0, N.view(work), piv.data_ptr(), N.view(x), N.LU_MODES["auto"])
+        return [("lu_factor (pivot-free chain + DMMA trailing updates)", 2 * n ** 3 // 3, factor),
+                ("lu_solve (DMMA wavefront, inverted diagonal blocks)", 2 * n * n * k, solve)]
 
     cpu_n = 1024
     cpu_sample_desc = "an n=1024 LU solve with 64 RHS (same unblocked algorithm; a rate, not the 8192 problem)"
