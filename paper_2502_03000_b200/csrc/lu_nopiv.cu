@@ -68,6 +68,8 @@ __global__ void __launch_bounds__(256) coldom_check(const double *__restrict__ A
 // shared memory, FMA arithmetic (tensor mode); 512 threads on a 2-D map (row
 // lane tx, column slice ty), one barrier pair per column.
 __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb) {
+    pdl_wait();  // launched with PDL: the previous chain kernel's output is the input
+    pdl_trigger();
     __shared__ double a[NBD * LDD];  // (i, j) at a[j * LDD + i]
     const int tid = threadIdx.x;
     const int tx = tid & (NBD - 1), ty = tid >> 6;
@@ -101,6 +103,8 @@ constexpr int kTriSmem = 2 * NBD * LDD * (int)sizeof(double);
 // leading dimension lda), U11 (nb x nb at U).  Row-wise substitution
 // x U = a:  x_i = s_i / u_ii;  s_j -= x_i u_ij (j > i)
 __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda, int64_t M, const double *U, int nb) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double tsm[];  // u_ij at tsm[j * LDD + i], j < 2 * NBD (zero past nb)
     __shared__ double rinv[NBD];     // 1 / u_ii: tensor mode multiplies (a division is 126 cycles of chain)
 #pragma unroll 16
@@ -132,6 +136,8 @@ __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda,
 // [0, N)), unit lower L11 (at L).  y_k final; y_i -= l_ik y_k (i > k)
 __global__ void __launch_bounds__(64) trsm_left_lower_unit(double *A12, int64_t lda, int64_t N, const double *L,
                                                           int nb) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ double tsm[];  // l_ik at tsm[k * LDD2 + i], i < 2 * NBD (zero past nb / on and above the diagonal)
     constexpr int LDD2 = 2 * NBD + 1;
 #pragma unroll 16
@@ -240,13 +246,14 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     constexpr int OB = 2 * NBD;
     auto trsm_ru = [&](double *A21, int64_t M, const double *U, int nb, cudaStream_t str) -> int {
         if (M <= 0) return 0;
-        trsm_right_upper<<<(unsigned)ceil_div(M, 64), 64, kTriSmem, str>>>(A21, lda, M, U, nb);
+        LM_CUDA(launch_pdl(trsm_right_upper, dim3((unsigned)ceil_div(M, 64)), dim3(64), kTriSmem, str, A21, lda, M, U, nb));
         LM_LAUNCHED(1);
         return 0;
     };
     auto trsm_ll = [&](double *A12, int64_t N, const double *L, int nb, cudaStream_t str) -> int {
         if (N <= 0) return 0;
-        trsm_left_lower_unit<<<(unsigned)ceil_div(N, 64), 64, kTriSmem + 8 * NBD, str>>>(A12, lda, N, L, nb);
+        LM_CUDA(launch_pdl(trsm_left_lower_unit, dim3((unsigned)ceil_div(N, 64)), dim3(64), kTriSmem + 8 * NBD, str, A12,
+                           lda, N, L, nb));
         LM_LAUNCHED(1);
         return 0;
     };
@@ -262,7 +269,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         const int nob = (int)(J1 - J0);
         double *Aaa = A + J0 + J0 * lda, *Abb = A + Ja + Ja * lda;
         // ---- factor the outer panel (columns J0..J1, rows J0..n) on hi
-        diag_nopiv<<<1, 512, 0, st.hi>>>(Aaa, lda, na);
+        LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(512), 0, st.hi, Aaa, lda, na));
         LM_LAUNCHED(1);
         mark(st.hi, 0);
         if (int rc = trsm_ru(A + Ja + J0 * lda, n - Ja, Aaa, na, st.hi)) return rc;  // L of block a, rows below a
@@ -273,7 +280,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
             if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + Ja * lda, lda, Abb, lda, n - Ja, nbb, na, st.hi))
                 return rc;
             mark(st.hi, 3);
-            diag_nopiv<<<1, 512, 0, st.hi>>>(Abb, lda, nbb);
+            LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(512), 0, st.hi, Abb, lda, nbb));
             LM_LAUNCHED(1);
             mark(st.hi, 0);
             if (int rc = trsm_ru(A + J1 + Ja * lda, n - J1, Abb, nbb, st.hi)) return rc;  // L of block b
