@@ -107,13 +107,20 @@ __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda,
     pdl_trigger();
     extern __shared__ double tsm[];  // u_ij at tsm[j * LDD + i], j < 2 * NBD (zero past nb)
     __shared__ double rinv[NBD];     // 1 / u_ii: tensor mode multiplies (a division is 126 cycles of chain)
-#pragma unroll 16
-    for (int e = threadIdx.x; e < 2 * NBD * NBD; e += blockDim.x) {
-        const int i = e & (NBD - 1), j = e >> 6;
-        tsm[j * LDD + i] = (i < nb && j < nb) ? U[i + (int64_t)j * lda] : (i == j && j < NBD ? 1.0 : 0.0);
+    // the nb x nb block: all of a thread's 64 loads in flight at once (16 at a
+    // time cost four L2 round trips on the panel chain), then the padding
+    {
+        const int i = threadIdx.x;  // blockDim.x == NBD
+        double u[NBD];
+#pragma unroll
+        for (int j = 0; j < NBD; ++j) u[j] = (i < nb && j < nb) ? U[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+#pragma unroll
+        for (int j = 0; j < NBD; ++j) {
+            tsm[j * LDD + i] = u[j];
+            tsm[(NBD + j) * LDD + i] = 0.0;
+        }
+        rinv[i] = i < nb ? 1.0 / U[i + (int64_t)i * lda] : 1.0;
     }
-    if (threadIdx.x < NBD)
-        rinv[threadIdx.x] = threadIdx.x < nb ? 1.0 / U[threadIdx.x + (int64_t)threadIdx.x * lda] : 1.0;
     __syncthreads();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= M) return;
@@ -140,10 +147,16 @@ __global__ void __launch_bounds__(64) trsm_left_lower_unit(double *A12, int64_t 
     pdl_trigger();
     extern __shared__ double tsm[];  // l_ik at tsm[k * LDD2 + i], i < 2 * NBD (zero past nb / on and above the diagonal)
     constexpr int LDD2 = 2 * NBD + 1;
-#pragma unroll 16
-    for (int e = threadIdx.x; e < NBD * 2 * NBD; e += blockDim.x) {
-        const int i = e % (2 * NBD), k = e / (2 * NBD);
-        tsm[k * LDD2 + i] = (i < nb && k < nb && i > k) ? L[i + (int64_t)k * lda] : 0.0;
+    {
+        const int i = threadIdx.x;  // blockDim.x == NBD: row i of L11, all loads in flight at once
+        double l[NBD];
+#pragma unroll
+        for (int k = 0; k < NBD; ++k) l[k] = (i < nb && k < nb && i > k) ? L[i + (int64_t)k * lda] : 0.0;
+#pragma unroll
+        for (int k = 0; k < NBD; ++k) {
+            tsm[k * LDD2 + i] = l[k];
+            tsm[k * LDD2 + NBD + i] = 0.0;
+        }
     }
     __syncthreads();
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
