@@ -68,11 +68,14 @@ __global__ void __launch_bounds__(256) coldom_check(const double *__restrict__ A
 // shared memory, FMA arithmetic (tensor mode), blocked by 8 columns: warp 0
 // factors the 64 x 8 panel in registers (two rows per lane, the pivot row
 // broadcast by shuffles, no barrier), 56 threads solve the panel's 8 rows of
-// U against L11 (8 x 8), then all 512 threads apply the rank-8 update --
-// three barriers per 8 columns.  (One rank-1 update and two barriers per
-// column took 28-42 us per block on the panel chain, 5.3 ms per 8192
-// factorisation.)
-__global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb) {
+// U against L11 (8 x 8), then all threads apply the rank-8 update -- three
+// barriers per 8 columns.  (One rank-1 update and two barriers per column
+// took 28-42 us per block on the panel chain, 5.3 ms per 8192 factorisation.)
+// 128 threads at <= 128 registers and 33 KB: the CTA fits next to three
+// resident trailing-update CTAs (46K registers, 170 KB) instead of waiting for
+// two of them to finish.
+constexpr int kDiagThreads = 128, kDiagSlices = kDiagThreads / NBD;
+__global__ void __launch_bounds__(kDiagThreads) diag_nopiv(double *A, int64_t lda, int nb) {
     pdl_wait();  // launched with PDL: the previous chain kernel's output is the input
     pdl_trigger();
     __shared__ double a[NBD * LDD];  // (i, j) at a[j * LDD + i]; identity outside nb x nb
@@ -80,7 +83,8 @@ __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int tx = tid & (NBD - 1), ty = tid >> 6;
 #pragma unroll
-    for (int c = ty; c < NBD; c += 8) a[c * LDD + tx] = (tx < nb && c < nb) ? A[tx + (int64_t)c * lda] : (tx == c ? 1.0 : 0.0);
+    for (int c = ty; c < NBD; c += kDiagSlices)
+        a[c * LDD + tx] = (tx < nb && c < nb) ? A[tx + (int64_t)c * lda] : (tx == c ? 1.0 : 0.0);
     __syncthreads();
 #pragma unroll 1
     for (int c0 = 0; c0 < NBD; c0 += PB) {
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb
             double l[PB];
 #pragma unroll
             for (int q = 0; q < PB; ++q) l[q] = a[(c0 + q) * LDD + tx];
-            for (int c = c1 + ty; c < NBD; c += 8) {
+            for (int c = c1 + ty; c < NBD; c += kDiagSlices) {
                 const double *u = a + c * LDD + c0;
                 double x = a[c * LDD + tx];
 #pragma unroll
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb
         }
         __syncthreads();
     }
-    for (int c = ty; c < nb; c += 8)
+    for (int c = ty; c < nb; c += kDiagSlices)
         if (tx < nb) A[tx + (int64_t)c * lda] = a[c * LDD + tx];
 }
 
@@ -154,8 +158,16 @@ __global__ void __launch_bounds__(512) diag_nopiv(double *A, int64_t lda, int nb
 // rolled with static register indices (the fully unrolled 64 x 64 solve is
 // ~8k instructions that every warp runs once: ncu showed 34% of the stalls
 // waiting on instruction fetch).  The triangle sits in shared memory padded
-// to 2 x 64 zero columns so entry i + j never leaves it.
-constexpr int kTriSmem = 2 * NBD * LDD * (int)sizeof(double);
+// with zero columns so entry i + j never leaves it; the step loop runs in two
+// halves -- steps 0..31 shift all 63 entries, steps 32..63 only the 31 that
+// can still be non-zero -- so i + j <= 94: 95 columns, 49 KB.  That fits next
+// to three resident trailing-update CTAs (the 128-column padding, 66.5 KB,
+// had to wait for one of them to finish), and the second half does half the
+// FMAs.
+constexpr int HNB = NBD / 2;
+constexpr int NPAD = NBD + HNB - 1;  // 95 columns (rows) of the padded triangle
+constexpr int kTriSmem = NPAD * LDD * (int)sizeof(double);        // trsm_right_upper: [NPAD columns][LDD]
+constexpr int kTriLowSmem = NBD * NPAD * (int)sizeof(double);     // trsm_left_lower_unit: [NBD columns][NPAD rows]
 
 // L21 = A21 U11^-1 in place: one thread per row of A21 (rows [0, M),
 // leading dimension lda), U11 (nb x nb at U).  Row-wise substitution
@@ -163,7 +175,7 @@ constexpr int kTriSmem = 2 * NBD * LDD * (int)sizeof(double);
 __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda, int64_t M, const double *U, int nb) {
     pdl_wait();
     pdl_trigger();
-    extern __shared__ double tsm[];  // u_ij at tsm[j * LDD + i], j < 2 * NBD (zero past nb)
+    extern __shared__ double tsm[];  // u_ij at tsm[j * LDD + i], j < NPAD (zero past nb)
     __shared__ double rinv[NBD];     // 1 / u_ii: tensor mode multiplies (a division is 126 cycles of chain)
     // the nb x nb block: all of a thread's 64 loads in flight at once (16 at a
     // time cost four L2 round trips on the panel chain), then the padding
@@ -173,10 +185,9 @@ __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda,
 #pragma unroll
         for (int j = 0; j < NBD; ++j) u[j] = (i < nb && j < nb) ? U[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
 #pragma unroll
-        for (int j = 0; j < NBD; ++j) {
-            tsm[j * LDD + i] = u[j];
-            tsm[(NBD + j) * LDD + i] = 0.0;
-        }
+        for (int j = 0; j < NBD; ++j) tsm[j * LDD + i] = u[j];
+#pragma unroll
+        for (int j = NBD; j < NPAD; ++j) tsm[j * LDD + i] = 0.0;
         rinv[i] = i < nb ? 1.0 / U[i + (int64_t)i * lda] : 1.0;
     }
     __syncthreads();
@@ -186,14 +197,24 @@ __global__ void __launch_bounds__(64) trsm_right_upper(double *A21, int64_t lda,
     double sv[NBD];
 #pragma unroll
     for (int c = 0; c < NBD; ++c) sv[c] = c < nb ? row[c * lda] : 0.0;
+    const int n1 = nb < HNB ? nb : HNB;
 #pragma unroll 1
-    for (int i = 0; i < nb; ++i) {
+    for (int i = 0; i < n1; ++i) {
         const double *ui = tsm + i;  // u_{i, i + j} at ui[(i + j) * LDD]
         const double x = sv[0] * rinv[i];
         row[i * lda] = x;
 #pragma unroll
         for (int j = 1; j < NBD; ++j) sv[j - 1] = fma(-x, ui[(i + j) * LDD], sv[j]);
         sv[NBD - 1] = 0.0;
+    }
+#pragma unroll 1
+    for (int i = HNB; i < nb; ++i) {  // entries i + j >= 64 do not exist: sv[32..] stays zero
+        const double *ui = tsm + i;
+        const double x = sv[0] * rinv[i];
+        row[i * lda] = x;
+#pragma unroll
+        for (int j = 1; j < HNB; ++j) sv[j - 1] = fma(-x, ui[(i + j) * LDD], sv[j]);
+        sv[HNB - 1] = 0.0;
     }
 }
 
@@ -203,8 +224,8 @@ __global__ void __launch_bounds__(64) trsm_left_lower_unit(double *A12, int64_t 
                                                           int nb) {
     pdl_wait();
     pdl_trigger();
-    extern __shared__ double tsm[];  // l_ik at tsm[k * LDD2 + i], i < 2 * NBD (zero past nb / on and above the diagonal)
-    constexpr int LDD2 = 2 * NBD + 1;
+    extern __shared__ double tsm[];  // l_ik at tsm[k * LDD2 + i], i < NPAD (zero past nb / on and above the diagonal)
+    constexpr int LDD2 = NPAD;  // 95: odd
     {
         const int i = threadIdx.x;  // blockDim.x == NBD: row i of L11, all loads in flight at once
         double l[NBD];
@@ -213,7 +234,7 @@ __global__ void __launch_bounds__(64) trsm_left_lower_unit(double *A12, int64_t 
 #pragma unroll
         for (int k = 0; k < NBD; ++k) {
             tsm[k * LDD2 + i] = l[k];
-            tsm[k * LDD2 + NBD + i] = 0.0;
+            if (i < NPAD - NBD) tsm[k * LDD2 + NBD + i] = 0.0;
         }
     }
     __syncthreads();
@@ -223,14 +244,24 @@ __global__ void __launch_bounds__(64) trsm_left_lower_unit(double *A12, int64_t 
     double y[NBD];
 #pragma unroll
     for (int i = 0; i < NBD; ++i) y[i] = i < nb ? col[i] : 0.0;
+    const int n1 = nb < HNB ? nb : HNB;
 #pragma unroll 1
-    for (int k = 0; k < nb; ++k) {
+    for (int k = 0; k < n1; ++k) {
         const double yk = y[0];
         col[k] = yk;
         const double *lk = tsm + k * LDD2 + k;  // l_{k + j, k} at lk[j]
 #pragma unroll
         for (int j = 1; j < NBD; ++j) y[j - 1] = fma(-lk[j], yk, y[j]);
         y[NBD - 1] = 0.0;
+    }
+#pragma unroll 1
+    for (int k = HNB; k < nb; ++k) {  // rows k + j >= 64 do not exist: y[32..] stays zero
+        const double yk = y[0];
+        col[k] = yk;
+        const double *lk = tsm + k * LDD2 + k;
+#pragma unroll
+        for (int j = 1; j < HNB; ++j) y[j - 1] = fma(-lk[j], yk, y[j]);
+        y[HNB - 1] = 0.0;
     }
 }
 
@@ -277,7 +308,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     NoPivStreams st;
     if (int rc = nopiv_streams(st)) return rc;
     if (int rc = func_attrs(trsm_right_upper, kTriSmem)) return rc;
-    if (int rc = func_attrs(trsm_left_lower_unit, kTriSmem + 8 * NBD)) return rc;
+    if (int rc = func_attrs(trsm_left_lower_unit, kTriLowSmem)) return rc;
     cudaEvent_t ev_fork, ev_l21, ev_rest, ev_join;
     LM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     LM_CUDA(cudaEventCreateWithFlags(&ev_l21, cudaEventDisableTiming));
@@ -323,7 +354,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     };
     auto trsm_ll = [&](double *A12, int64_t N, const double *L, int nb, cudaStream_t str) -> int {
         if (N <= 0) return 0;
-        LM_CUDA(launch_pdl(trsm_left_lower_unit, dim3((unsigned)ceil_div(N, 64)), dim3(64), kTriSmem + 8 * NBD, str, A12,
+        LM_CUDA(launch_pdl(trsm_left_lower_unit, dim3((unsigned)ceil_div(N, 64)), dim3(64), kTriLowSmem, str, A12,
                            lda, N, L, nb));
         LM_LAUNCHED(1);
         return 0;
@@ -340,7 +371,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         const int nob = (int)(J1 - J0);
         double *Aaa = A + J0 + J0 * lda, *Abb = A + Ja + Ja * lda;
         // ---- factor the outer panel (columns J0..J1, rows J0..n) on hi
-        LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(512), 0, st.hi, Aaa, lda, na));
+        LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(kDiagThreads), 0, st.hi, Aaa, lda, na));
         LM_LAUNCHED(1);
         mark(st.hi, 0);
         if (int rc = trsm_ru(A + Ja + J0 * lda, n - Ja, Aaa, na, st.hi)) return rc;  // L of block a, rows below a
@@ -351,7 +382,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
             if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + Ja * lda, lda, Abb, lda, n - Ja, nbb, na, st.hi))
                 return rc;
             mark(st.hi, 3);
-            LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(512), 0, st.hi, Abb, lda, nbb));
+            LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(kDiagThreads), 0, st.hi, Abb, lda, nbb));
             LM_LAUNCHED(1);
             mark(st.hi, 0);
             if (int rc = trsm_ru(A + J1 + Ja * lda, n - J1, Abb, nbb, st.hi)) return rc;  // L of block b
