@@ -309,17 +309,20 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     if (int rc = nopiv_streams(st)) return rc;
     if (int rc = func_attrs(trsm_right_upper, kTriSmem)) return rc;
     if (int rc = func_attrs(trsm_left_lower_unit, kTriLowSmem)) return rc;
-    cudaEvent_t ev_fork, ev_l21, ev_rest, ev_join;
+    cudaEvent_t ev_fork, ev_l21, ev_rest, ev_join, ev_da, ev_ra, ev_db;
     LM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     LM_CUDA(cudaEventCreateWithFlags(&ev_l21, cudaEventDisableTiming));
     LM_CUDA(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
     LM_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_da, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_ra, cudaEventDisableTiming));
+    LM_CUDA(cudaEventCreateWithFlags(&ev_db, cudaEventDisableTiming));
     struct EvGuard {
-        cudaEvent_t e[4];
+        cudaEvent_t e[7];
         ~EvGuard() {
             for (auto x : e) cudaEventDestroy(x);
         }
-    } guard{{ev_fork, ev_l21, ev_rest, ev_join}};
+    } guard{{ev_fork, ev_l21, ev_rest, ev_join, ev_da, ev_ra, ev_db}};
     LM_CUDA(cudaEventRecord(ev_fork, s));
     LM_CUDA(cudaStreamWaitEvent(st.hi, ev_fork, 0));
     LM_CUDA(cudaStreamWaitEvent(st.lo, ev_fork, 0));
@@ -363,6 +366,8 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     // opt-in (LM_NOPIV_SPLIT=1): measured slower on config 4a, 28.6 vs 27.9 ms -- the
     // low-priority stream's GEMM work, not the panel chain's wait, bounds the step
     static const bool split_rest = getenv("LM_NOPIV_SPLIT") && getenv("LM_NOPIV_SPLIT")[0] == '1';
+    // opt-in (LM_NOPIV_EARLY=1): measured neutral on config 4a (25.70 vs 25.71-25.79 ms)
+    static const bool early_u12 = getenv("LM_NOPIV_EARLY") && getenv("LM_NOPIV_EARLY")[0] == '1';
     for (int64_t J0 = 0; J0 < n; J0 += OB) {
         const int na = (int)((n - J0) < NBD ? (n - J0) : NBD);
         const int64_t Ja = J0 + na;
@@ -370,13 +375,35 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         const int64_t J1 = Ja + nbb, J2 = (J1 + OB) < n ? J1 + OB : n;
         const int nob = (int)(J1 - J0);
         double *Aaa = A + J0 + J0 * lda, *Abb = A + Ja + Ja * lda;
-        // ---- factor the outer panel (columns J0..J1, rows J0..n) on hi
+        // ---- factor the outer panel (columns J0..J1, rows J0..n) on hi.  The
+        // low-priority stream's U12 solves of the remaining columns need only
+        // the diagonal factors (and L_ba), not the whole L21: they are issued
+        // as soon as those exist, so after ev_l21 only the trailing GEMM is
+        // left on that stream (opt-in, LM_NOPIV_EARLY=1; default: all of it after ev_l21).
+        const int64_t nn2 = n - J2;
+        const bool early = early_u12 && nn2 > 0;
         LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(kDiagThreads), 0, st.hi, Aaa, lda, na));
         LM_LAUNCHED(1);
         mark(st.hi, 0);
+        if (early) {
+            LM_CUDA(cudaEventRecord(ev_da, st.hi));
+            LM_CUDA(cudaStreamWaitEvent(st.lo, ev_da, 0));
+            mark(st.lo, 6);
+            if (int rc = trsm_ll(A + J0 + J2 * lda, nn2, Aaa, na, st.lo)) return rc;  // U12, rows of block a
+            mark(st.lo, 7);
+        }
         if (int rc = trsm_ru(A + Ja + J0 * lda, n - Ja, Aaa, na, st.hi)) return rc;  // L of block a, rows below a
         mark(st.hi, 1);
         if (nbb > 0) {
+            if (early) {
+                LM_CUDA(cudaEventRecord(ev_ra, st.hi));
+                LM_CUDA(cudaStreamWaitEvent(st.lo, ev_ra, 0));
+                mark(st.lo, 6);
+                if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + J2 * lda, lda, A + Ja + J2 * lda, lda, nbb, nn2,
+                                       na, st.lo))
+                    return rc;
+                mark(st.lo, 7);
+            }
             if (int rc = trsm_ll(A + J0 + Ja * lda, nbb, Aaa, na, st.hi)) return rc;  // U_ab
             mark(st.hi, 2);
             if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + Ja * lda, lda, Abb, lda, n - Ja, nbb, na, st.hi))
@@ -385,6 +412,13 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
             LM_CUDA(launch_pdl(diag_nopiv, dim3(1), dim3(kDiagThreads), 0, st.hi, Abb, lda, nbb));
             LM_LAUNCHED(1);
             mark(st.hi, 0);
+            if (early) {
+                LM_CUDA(cudaEventRecord(ev_db, st.hi));
+                LM_CUDA(cudaStreamWaitEvent(st.lo, ev_db, 0));
+                mark(st.lo, 6);
+                if (int rc = trsm_ll(A + Ja + J2 * lda, nn2, Abb, nbb, st.lo)) return rc;  // U12, rows of block b
+                mark(st.lo, 7);
+            }
             if (int rc = trsm_ru(A + J1 + Ja * lda, n - J1, Abb, nbb, st.hi)) return rc;  // L of block b
             mark(st.hi, 1);
         }
@@ -393,9 +427,12 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         // ---- U12 of the outer block's rows over the columns [c0, c0 + nc), then
         // the rank-nob update of the rows below
         auto u12 = [&](int64_t c0, int64_t nc, cudaStream_t str, bool hi) -> int {
-            if (int rc = trsm_ll(A + J0 + c0 * lda, nc, Aaa, na, str)) return rc;
-            mark(str, hi ? 2 : 7);
-            if (nbb > 0) {
+            const bool solved = !hi && early;  // the U12 solves were issued above
+            if (!solved) {
+                if (int rc = trsm_ll(A + J0 + c0 * lda, nc, Aaa, na, str)) return rc;
+                mark(str, hi ? 2 : 7);
+            }
+            if (nbb > 0 && !solved) {
                 if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + c0 * lda, lda, A + Ja + c0 * lda, lda, nbb, nc,
                                        na, str))
                     return rc;
@@ -420,7 +457,6 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         };
         // the remaining columns on the low-priority stream (after the previous
         // outer block's, which wrote the same columns)
-        const int64_t nn2 = n - J2;
         // the next outer panel's columns were last written by the first piece
         // of the previous block's trailing update (ev_rest, recorded inside
         // u12): the wait is enqueued before this block's update re-records it
