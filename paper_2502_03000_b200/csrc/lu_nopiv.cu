@@ -27,6 +27,7 @@
 // reference computes for these matrices.
 #include <chrono>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -265,6 +266,109 @@ __global__ void __launch_bounds__(64) trsm_left_lower_unit(double *A12, int64_t 
     }
 }
 
+// U12 of a whole outer block in ONE launch (both inner blocks full): with
+// L = [[L_aa, 0], [L_ba, L_bb]] (128 x 128 unit lower, at Lob), per column
+//   y_a = L_aa^-1 a_a;   a_b -= L_ba y_a;   y_b = L_bb^-1 a_b
+// -- what trsm_left_lower_unit, the 64 x N x 64 product and a second
+// trsm_left_lower_unit did as three dependent launches on the panel chain.
+// One thread per column; the three operators take turns in the same shared
+// memory; y_a is re-read from the column (16 values at a time) for the
+// middle step, so the footprint stays that of trsm_left_lower_unit.
+__global__ void __launch_bounds__(64) trsm_left_lower_pair(double *A12, int64_t lda, int64_t N, const double *Lob) {
+    pdl_wait();
+    pdl_trigger();
+    extern __shared__ double tsm[];
+    constexpr int LDD2 = NPAD;
+    const int t = threadIdx.x;  // blockDim.x == NBD
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + t;
+    const bool live = c < N;
+    double *col = A12 + (live ? c : 0) * lda;
+    double y[NBD];
+    // strictly lower part of the 64 x 64 block at L, zero-padded rows; CH loads
+    // in flight at a time (32 while y is live: 64 + 2 x 64 registers spill)
+    auto load_tri = [&](const double *L, auto ch) {
+        constexpr int CH = decltype(ch)::value;
+#pragma unroll
+        for (int k0 = 0; k0 < NBD; k0 += CH) {
+            double l[CH];
+#pragma unroll
+            for (int k = 0; k < CH; ++k) l[k] = t > k0 + k ? L[t + (int64_t)(k0 + k) * lda] : 0.0;
+#pragma unroll
+            for (int k = 0; k < CH; ++k) {
+                tsm[(k0 + k) * LDD2 + t] = l[k];
+                if (t < NPAD - NBD) tsm[(k0 + k) * LDD2 + NBD + t] = 0.0;
+            }
+        }
+    };
+    auto solve = [&](double *dst) {  // y <- L^-1 y, step by step into dst[0..63]
+#pragma unroll 1
+        for (int k = 0; k < HNB; ++k) {
+            const double yk = y[0];
+            dst[k] = yk;
+            const double *lk = tsm + k * LDD2 + k;
+#pragma unroll
+            for (int j = 1; j < NBD; ++j) y[j - 1] = fma(-lk[j], yk, y[j]);
+            y[NBD - 1] = 0.0;
+        }
+#pragma unroll 1
+        for (int k = HNB; k < NBD; ++k) {
+            const double yk = y[0];
+            dst[k] = yk;
+            const double *lk = tsm + k * LDD2 + k;
+#pragma unroll
+            for (int j = 1; j < HNB; ++j) y[j - 1] = fma(-lk[j], yk, y[j]);
+            y[HNB - 1] = 0.0;
+        }
+    };
+    load_tri(Lob, std::integral_constant<int, 32>{});
+#pragma unroll
+    for (int i = 0; i < NBD; ++i) y[i] = live ? col[i] : 0.0;
+    __syncthreads();
+    if (live) solve(col);
+    __syncthreads();
+    // L_ba (64 x 64, dense) -> tsm[k * NBD + i]; a_b - L_ba y_a -> y
+#pragma unroll
+    for (int k0 = 0; k0 < NBD; k0 += 32) {
+        double l[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) l[k] = Lob[NBD + t + (int64_t)(k0 + k) * lda];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) tsm[(k0 + k) * NBD + t] = l[k];
+    }
+    __syncthreads();
+    // 32 outputs at a time (y_a, 16 values per batch, + 64 outputs + the
+    // operator's values in flight would spill); the results go back to the
+    // column and are re-read for the second solve
+    if (live) {
+#pragma unroll 1
+        for (int h = 0; h < NBD; h += HNB) {
+            double z[HNB];
+#pragma unroll
+            for (int i = 0; i < HNB; ++i) z[i] = col[NBD + h + i];
+#pragma unroll 1
+            for (int k0 = 0; k0 < NBD; k0 += 16) {
+                double ya[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) ya[q] = col[k0 + q];  // (this thread's own stores)
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const double *lk = tsm + (k0 + q) * NBD + h;
+#pragma unroll
+                    for (int i = 0; i < HNB; ++i) z[i] = fma(-lk[i], ya[q], z[i]);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < HNB; ++i) col[NBD + h + i] = z[i];
+        }
+    }
+    __syncthreads();
+    load_tri(Lob + NBD + (int64_t)NBD * lda, std::integral_constant<int, 32>{});
+#pragma unroll
+    for (int i = 0; i < NBD; ++i) y[i] = live ? col[NBD + i] : 0.0;
+    __syncthreads();
+    if (live) solve(col + NBD);
+}
+
 // max |l_ij| over the strictly lower triangle of the n x n factor (bit pattern
 // of a non-negative double orders like the value)
 __global__ void __launch_bounds__(256) lower_absmax(const double *__restrict__ A, int64_t n, int64_t lda,
@@ -309,6 +413,7 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     if (int rc = nopiv_streams(st)) return rc;
     if (int rc = func_attrs(trsm_right_upper, kTriSmem)) return rc;
     if (int rc = func_attrs(trsm_left_lower_unit, kTriLowSmem)) return rc;
+    if (int rc = func_attrs(trsm_left_lower_pair, kTriLowSmem)) return rc;
     cudaEvent_t ev_fork, ev_l21, ev_rest, ev_join, ev_da, ev_ra, ev_db;
     LM_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     LM_CUDA(cudaEventCreateWithFlags(&ev_l21, cudaEventDisableTiming));
@@ -366,6 +471,8 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
     // opt-in (LM_NOPIV_SPLIT=1): measured slower on config 4a, 28.6 vs 27.9 ms -- the
     // low-priority stream's GEMM work, not the panel chain's wait, bounds the step
     static const bool split_rest = getenv("LM_NOPIV_SPLIT") && getenv("LM_NOPIV_SPLIT")[0] == '1';
+    // opt-in (LM_NOPIV_PAIR=1): measured neutral on config 4a (25.59 vs 25.51-25.54 ms)
+    static const bool pair_u12 = getenv("LM_NOPIV_PAIR") && getenv("LM_NOPIV_PAIR")[0] == '1';
     // opt-in (LM_NOPIV_EARLY=1): measured neutral on config 4a (25.70 vs 25.71-25.79 ms)
     static const bool early_u12 = getenv("LM_NOPIV_EARLY") && getenv("LM_NOPIV_EARLY")[0] == '1';
     for (int64_t J0 = 0; J0 < n; J0 += OB) {
@@ -428,11 +535,18 @@ int nopiv_factor(double *A, int64_t n, int64_t lda, cudaStream_t s) {
         // the rank-nob update of the rows below
         auto u12 = [&](int64_t c0, int64_t nc, cudaStream_t str, bool hi) -> int {
             const bool solved = !hi && early;  // the U12 solves were issued above
-            if (!solved) {
+            const bool pair = !solved && pair_u12 && na == NBD && nbb == NBD;
+            if (pair) {  // both solves and the product between them in one launch
+                LM_CUDA(launch_pdl(trsm_left_lower_pair, dim3((unsigned)ceil_div(nc, 64)), dim3(64), kTriLowSmem, str,
+                                   A + J0 + c0 * lda, lda, nc, Aaa));
+                LM_LAUNCHED(1);
+                mark(str, hi ? 2 : 7);
+            }
+            if (!solved && !pair) {
                 if (int rc = trsm_ll(A + J0 + c0 * lda, nc, Aaa, na, str)) return rc;
                 mark(str, hi ? 2 : 7);
             }
-            if (nbb > 0 && !solved) {
+            if (nbb > 0 && !solved && !pair) {
                 if (int rc = dgemm_sub(A + Ja + J0 * lda, lda, A + J0 + c0 * lda, lda, A + Ja + c0 * lda, lda, nbb, nc,
                                        na, str))
                     return rc;
