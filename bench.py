@@ -598,9 +598,8 @@ class Config4a(Workload):
         piv = torch.empty(n, dtype=torch.int64, device=A.device)
         info = torch.zeros(1, dtype=torch.int32, device=A.device)
 
-        def factor():  # (the 537 MB workspace copy is 0.3% of the factorisation)
-            work.copy_(A)
-            N.call("lm_lu_factor", 0, N.view(work), piv.data_ptr(), info.data_ptr())
+        def factor():  # (out of place, as _lu_factor: the 537 MB workspace copy is inside the call)
+            N.call("lm_lu_factor_from", 0, N.view(A), N.view(work), piv.data_ptr(), info.data_ptr(), N.LU_MODES["auto"])
 
         def solve():
             x.copy_(b)

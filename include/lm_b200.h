@@ -142,6 +142,11 @@ int lm_lu_factor(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_info, void *s
  * tensor from there on, overridable with LM_LU_MODE=exact|tensor. */
 enum { LM_LU_AUTO = 0, LM_LU_EXACT = 1, LM_LU_TENSOR = 2 };
 int lm_lu_factor_mode(int dtype, lm_view lu, int64_t *d_piv, int32_t *d_info, int mode, void *stream);
+/* Out-of-place form, the shape of _lu_factor itself (lazymat/_loops.py:200-236
+ * copies its argument): src (F-order, left untouched) is copied into lu and
+ * factored there.  The pivot-free path uses src as its restore point instead
+ * of keeping a backup copy (n x n doubles of scratch and one more pass). */
+int lm_lu_factor_from(int dtype, lm_view src, lm_view lu, int64_t *d_piv, int32_t *d_info, int mode, void *stream);
 /* Solve with a factorisation from lm_lu_factor; x (n x m, F-order)
  * arrives holding B and is overwritten with X. */
 int lm_lu_solve(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, void *stream);

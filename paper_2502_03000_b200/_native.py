@@ -32,7 +32,7 @@ EXPORTS = (
     "lm_fused_axpby", "lm_fused_program", "lm_program_source", "lm_copy", "lm_vec_sum",
     "lm_gemm", "lm_gemm_chain", "lm_gemv", "lm_syrk",
     "lm_diag_scale", "lm_diag_of_product", "lm_trace_of_product", "lm_triple_diag_dot",
-    "lm_analyze", "lm_lu_factor", "lm_lu_factor_mode", "lm_lu_solve", "lm_lu_solve_mode", "lm_band_solve", "lm_tri_solve",
+    "lm_analyze", "lm_lu_factor", "lm_lu_factor_mode", "lm_lu_factor_from", "lm_lu_solve", "lm_lu_solve_mode", "lm_band_solve", "lm_tri_solve",
     "lm_transpose_copy", "lm_diag_materialise", "lm_set_identity",
     "lm_lu_solve_batched", "lm_solve_batched_classified", "lm_solve_batched_classified_from", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
     "lm_fill_pcg64", "lm_nccl_load", "lm_nccl_unique_id", "lm_nccl_init_rank", "lm_nccl_init_all",
@@ -72,6 +72,7 @@ _SIGS = {
     "lm_analyze": (_i, [_i, View, _i, _p, _p]),
     "lm_lu_factor": (_i, [_i, View, _p, _p, _p]),
     "lm_lu_factor_mode": (_i, [_i, View, _p, _p, _i, _p]),
+    "lm_lu_factor_from": (_i, [_i, View, View, _p, _p, _i, _p]),
     "lm_lu_solve": (_i, [_i, View, _p, View, _p]),
     "lm_lu_solve_mode": (_i, [_i, View, _p, View, _i, _p]),
     "lm_band_solve": (_i, [_i, View, View, _i64, _i64, _p, _p, _p, _p]),

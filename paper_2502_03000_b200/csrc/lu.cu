@@ -346,7 +346,8 @@ int launch_trsm(const double *T, int64_t ldt, double *X, int64_t ldx, int nbj, i
 constexpr int kLuNb = 64;
 
 int lu_factor_fast(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, bool tensor);
-int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s);
+int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, const double *orig,
+                    int64_t ldo);
 int lu_solve_wavefront(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s,
                        const int *only_if);
 int lu_solve_tensor(const double *LU, int64_t n, int64_t lda, double *X, int64_t ldx, int64_t m, cudaStream_t s);
@@ -375,7 +376,8 @@ static bool lu_tensor_mode(int mode, int64_t n) {
     return n >= LU_TENSOR_MIN_N;
 }
 
-int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, int mode) {
+int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, int mode,
+                   const double *orig = nullptr, int64_t ldo = 0) {
     LM_CUDA(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     if (n == 0) return 0;
     // two-level blocked LU with a thread-block-cluster panel (lu_fast.cu);
@@ -385,7 +387,7 @@ int lu_factor_impl(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *inf
     // tensor mode, column diagonally dominant A: partial pivoting provably
     // never swaps -> the pivot-free, all-GEMM factorisation (lu_nopiv.cu)
     if (tensor)
-        if (int rc = lu_factor_nopiv(A, n, lda, piv, info, s); rc != 1) return rc;
+        if (int rc = lu_factor_nopiv(A, n, lda, piv, info, s, orig, ldo); rc != 1) return rc;
     if (int rc = lu_factor_fast(A, n, lda, piv, info, s, tensor); rc != 1) return rc;
     const int nsm = num_sms();
     Scratch pub;
@@ -718,6 +720,23 @@ extern "C" int lm_lu_factor_mode(int dtype, lm_view lu, int64_t *d_piv, int32_t 
     LM_REQUIRE(lu.rows == lu.cols, "lu_factor needs a square matrix");
     LM_REQUIRE(lu.rs == 1 && (lu.cs >= lu.rows || lu.rows <= 1), "lu_factor needs F-order storage");
     return lu_factor_impl((double *)lu.ptr, lu.rows, lu.cs > 0 ? lu.cs : 1, d_piv, d_info, as_stream(stream), mode);
+}
+
+extern "C" int lm_lu_factor_from(int dtype, lm_view src, lm_view lu, int64_t *d_piv, int32_t *d_info, int mode,
+                                 void *stream) {
+    clear_error();
+    LM_REQUIRE(dtype == LM_F64, "lu_factor: f64 only");
+    LM_REQUIRE(mode == LM_LU_AUTO || mode == LM_LU_EXACT || mode == LM_LU_TENSOR, "lu_factor: bad mode %d", mode);
+    LM_REQUIRE(lu.rows == lu.cols && src.rows == lu.rows && src.cols == lu.cols, "lu_factor needs square matrices of one size");
+    LM_REQUIRE(lu.rs == 1 && (lu.cs >= lu.rows || lu.rows <= 1), "lu_factor needs F-order storage");
+    LM_REQUIRE(src.rs == 1 && (src.cs >= src.rows || src.rows <= 1), "lu_factor_from needs an F-order source");
+    LM_REQUIRE(src.ptr != lu.ptr, "lu_factor_from: source and workspace must differ");
+    cudaStream_t s = as_stream(stream);
+    const int64_t n = lu.rows, lda = lu.cs > 0 ? lu.cs : 1, ldo = src.cs > 0 ? src.cs : 1;
+    if (n > 0)
+        LM_CUDA(cudaMemcpy2DAsync(lu.ptr, lda * sizeof(double), src.ptr, ldo * sizeof(double), n * sizeof(double), n,
+                                  cudaMemcpyDeviceToDevice, s));
+    return lu_factor_impl((double *)lu.ptr, n, lda, d_piv, d_info, s, mode, (const double *)src.ptr, ldo);
 }
 
 extern "C" int lm_lu_solve(int dtype, lm_view lu, const int64_t *d_piv, lm_view x, void *stream) {

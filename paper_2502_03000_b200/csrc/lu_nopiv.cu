@@ -623,8 +623,11 @@ bool lu_nopiv_enabled() {
 // 0: factored without swaps (piv = identity, *info = 0); 1: not applicable
 // (A is not column-dominant, or a multiplier came out too close to 1 and A
 // was restored) -- the caller runs the pivoting LU; < 0: error.
-// Synchronises s twice (the dominance and the multiplier checks).
-int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s) {
+// Synchronises s twice (the dominance and the multiplier checks).  orig (may
+// be null): an untouched copy of the matrix the caller still holds (leading
+// dimension ldo) -- then no backup is made (a 537 MB copy at n = 8192).
+int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *info, cudaStream_t s, const double *orig,
+                    int64_t ldo) {
     if (n < 2 || !lu_nopiv_enabled()) return 1;
     Scratch flags;
     if (int rc = flags.alloc(16, s)) return rc;
@@ -638,9 +641,13 @@ int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *in
     LM_CUDA(cudaStreamSynchronize(s));
     if (h_flag) return 1;
     Scratch backup;  // the original matrix, in case the multiplier check fails
-    if (int rc = backup.alloc(sizeof(double) * (size_t)n * n, s)) return rc;
-    LM_CUDA(cudaMemcpy2DAsync(backup.p, n * sizeof(double), A, lda * sizeof(double), n * sizeof(double), n,
-                              cudaMemcpyDeviceToDevice, s));
+    if (!orig) {
+        if (int rc = backup.alloc(sizeof(double) * (size_t)n * n, s)) return rc;
+        LM_CUDA(cudaMemcpy2DAsync(backup.p, n * sizeof(double), A, lda * sizeof(double), n * sizeof(double), n,
+                                  cudaMemcpyDeviceToDevice, s));
+        orig = backup.as<double>();
+        ldo = n;
+    }
     if (int rc = nopiv_factor(A, n, lda, s)) return rc;
     lower_absmax<<<(unsigned)(4 * num_sms()), 256, 0, s>>>(A, n, lda, d_max);
     LM_LAUNCHED(1);
@@ -650,7 +657,7 @@ int lu_factor_nopiv(double *A, int64_t n, int64_t lda, int64_t *piv, int32_t *in
     double mx;
     memcpy(&mx, &h_max, sizeof(mx));
     if (!(mx < kMulBound)) {  // not provably the reference's pivots: restore, let the caller pivot
-        LM_CUDA(cudaMemcpy2DAsync(A, lda * sizeof(double), backup.p, n * sizeof(double), n * sizeof(double), n,
+        LM_CUDA(cudaMemcpy2DAsync(A, lda * sizeof(double), orig, ldo * sizeof(double), n * sizeof(double), n,
                                   cudaMemcpyDeviceToDevice, s));
         return 1;
     }

@@ -494,6 +494,29 @@ def test_lu_solve_rhs_groups_bitwise(n, m):
     assert bits_equal(host(x), x_ref)
 
 
+@pytest.mark.parametrize("n,kind,mode", [(200, "general", "exact"), (333, "dominant", "exact"),
+                                         (2048, "dominant", "tensor"), (2048, "general", "tensor")])
+def test_lu_factor_from_equals_in_place(n, kind, mode):
+    """lm_lu_factor_from (out of place, the shape of _lu_factor) = copy +
+    lm_lu_factor_mode bit for bit, pivot-free path included (it restores from
+    the source instead of a backup), and the source stays untouched."""
+    from paper_2502_03000_b200 import _native as N
+    rng = np.random.default_rng(n + 5)
+    a = np.asfortranarray(rng.uniform(-1, 1, (n + 3, n))[:n, :] + (n * np.eye(n) if kind == "dominant" else 0))
+    big = dev(np.asfortranarray(np.vstack([a, np.zeros((3, n))])))  # leading dimension n + 3
+    src = big[:n, :]
+    keep = src.clone()
+    lu1, lu2 = fortran_empty(n, n, device=DEV), fortran_empty(n, n, device=DEV)
+    piv1, piv2 = (torch.empty(n, dtype=torch.int64, device=DEV) for _ in range(2))
+    info = torch.zeros(1, dtype=torch.int32, device=DEV)
+    N.call("lm_lu_factor_from", 0, N.view(src), N.view(lu1), piv1.data_ptr(), info.data_ptr(), N.LU_MODES[mode])
+    assert int(info.item()) == 0
+    lu2.copy_(src)
+    N.call("lm_lu_factor_mode", 0, N.view(lu2), piv2.data_ptr(), info.data_ptr(), N.LU_MODES[mode])
+    assert torch.equal(src, keep)
+    assert torch.equal(piv1, piv2) and torch.equal(lu1, lu2)
+
+
 def _scaled_residual(a, x, b):
     return np.linalg.norm(a @ x - b, np.inf) / (np.linalg.norm(a, np.inf) * np.linalg.norm(x, np.inf) +
                                                 np.linalg.norm(b, np.inf))
