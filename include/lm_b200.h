@@ -254,6 +254,9 @@ int lm_fill_pcg64(int dtype, void *out, int64_t batch, int64_t rows, int64_t col
  * column and phase (4 per column) into d_clock (tools/panel_probe.py). */
 int lm_debug_lu_panel(lm_view a, int64_t j0, int nb, int64_t *d_piv, int32_t *d_info, long long *d_clock,
                       void *stream);
+/* Diagnostics: c -= a b through the blocked LU's trailing-update GEMM (F-order
+ * operands; tools/gemm_sub_probe.py times the kernel on config 4a's shapes). */
+int lm_debug_gemm_sub(lm_view a, lm_view b, lm_view c, void *stream);
 
 #ifdef __cplusplus
 }

@@ -37,7 +37,7 @@ EXPORTS = (
     "lm_lu_solve_batched", "lm_solve_batched_classified", "lm_solve_batched_classified_from", "lm_analyze_batched", "lm_expr_atb_schur_trace_batched", "lm_fill_uniform",
     "lm_fill_pcg64", "lm_nccl_load", "lm_nccl_unique_id", "lm_nccl_init_rank", "lm_nccl_init_all",
     "lm_allreduce_sum", "lm_allreduce_sum_f64", "lm_nccl_destroy",
-    "lm_debug_lu_panel",
+    "lm_debug_lu_panel", "lm_debug_gemm_sub",
 )
 
 
@@ -96,6 +96,7 @@ _SIGS = {
     "lm_allreduce_sum_f64": (_i, [_p, _p, _p]),
     "lm_nccl_destroy": (_i, [_p]),
     "lm_debug_lu_panel": (_i, [View, _i64, _i, _p, _p, _p, _p]),
+    "lm_debug_gemm_sub": (_i, [View, View, View, _p]),
 }
 
 _lock = threading.Lock()

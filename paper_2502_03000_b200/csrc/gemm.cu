@@ -1151,6 +1151,14 @@ extern "C" int lm_gemm(int dtype, lm_view a, lm_view b, lm_view out, void *strea
     return -1;
 }
 
+extern "C" int lm_debug_gemm_sub(lm_view a, lm_view b, lm_view c, void *stream) {
+    clear_error();
+    LM_REQUIRE(a.cols == b.rows && c.rows == a.rows && c.cols == b.cols, "gemm_sub shape mismatch");
+    LM_REQUIRE(a.rs == 1 && b.rs == 1 && c.rs == 1, "gemm_sub needs F-order operands");
+    return dgemm_sub((const double *)a.ptr, a.cs, (const double *)b.ptr, b.cs, (double *)c.ptr, c.cs, a.rows, b.cols,
+                     a.cols, as_stream(stream));
+}
+
 extern "C" int lm_syrk(int dtype, lm_view a, lm_view out, void *stream) {
     clear_error();
     LM_REQUIRE(out.rows == a.rows && out.cols == a.rows, "syrk out shape mismatch");
