@@ -467,7 +467,8 @@ template <bool CONTIG_OUTER, int BKT> constexpr int stage_doubles() {
 // (mma.sync.m8n8k4.f64).  4 warps in 2 x 2, warp tile 32 x 32 (16 DMMA
 // accumulators), ST-stage cp.async ring with one barrier per K step.
 template <bool A_CM, bool B_CN, bool VA, bool VB, int BKT, int ST>
-__global__ void __launch_bounds__(kGmThreads) dgemm_dmma(GemmArgs g) {
+// (launch bounds: 4 CTAs per SM at <= 128 registers for the 3-stage ring, 5 at <= 102 for the 2-stage one)
+__global__ void __launch_bounds__(kGmThreads, ST == 2 ? 5 : 4) dgemm_dmma(GemmArgs g) {
     pdl_wait();  // inputs may be the previous kernel's output (PDL)
     pdl_trigger();
     extern __shared__ __align__(16) double gsm[];
@@ -1066,6 +1067,14 @@ int dgemm_sub(const double *a, int64_t lda, const double *b, int64_t ldb, double
     auto aligned16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
     const bool va = aligned16(a) && lda % 2 == 0;
     const bool vb = aligned16(b) && ldb % 2 == 0;
+    // Wide trailing updates (more than 128 columns): the 2-stage ring at <= 102
+    // registers, five resident CTAs per SM instead of four (the kernel is bound
+    // by how many CTAs overlap their loads, barriers and read-modify-write
+    // epilogues: 20.8 -> 23.9 TF/s alone, tools/gemm_sub_probe.py; config 4a
+    // 25.95 -> 24.6 ms; deeper rings / BK = 32 at 2-3 CTAs per SM: 12-18 TF/s).
+    // Same tiles, same K order: bit-identical.  LM_GEMM_SUB_CFG=163: the 3-stage ring.
+    static const bool ring3 = getenv("LM_GEMM_SUB_CFG") && atoi(getenv("LM_GEMM_SUB_CFG")) == 163;
+    if (N > 128 && !ring3) return dgemm_cfg<16, 2>(g, true, false, va, vb, s);
     return dgemm_cfg<16, 3>(g, true, false, va, vb, s);
 }
 
