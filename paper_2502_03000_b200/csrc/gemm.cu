@@ -510,6 +510,20 @@ __global__ void __launch_bounds__(kGmThreads, ST == 2 ? 5 : 4) dgemm_dmma(GemmAr
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (m0 + wm + i * 8 < g.M && n0 + wn + j * 8 < g.N) live |= 1u << (4 * i + j);
+    // C -= A B reads its C tile only in the epilogue, from HBM (the LU's
+    // trailing matrix does not fit L2): ask for the lines now, one request per
+    // 64-byte fragment column, so the epilogue's loads find them in L2
+    if (g.sub && g.c_sm == 1 && fr == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t m = m0 + wm + i * 8, n = n0 + wn + j * 8 + 2 * fc + h;
+                    if (m < g.M && n < g.N) asm volatile("prefetch.global.L2 [%0];" ::"l"(g.c + m + n * g.c_sn));
+                }
+    }
     TileStream<A_CM, VA, BKT> ta;
     TileStream<B_CN, VB, BKT> tb;
     ta.init(g.a, g.a_sm, g.a_sk, m0, kb);
