@@ -569,6 +569,28 @@ __global__ void __launch_bounds__(kGmThreads, ST == 2 ? 5 : 4) dgemm_dmma(GemmAr
                     dmma(acc[i][j], af[i], bf[j]);
         }
     }
+    // C -= A B on an F-order C with even rows / leading dimension: lanes fr and
+    // fr ^ 1 trade one accumulator so that each owns two consecutive rows of one
+    // column -- 16-byte read-modify-writes, half the memory instructions
+    if (g.sub && g.c_sm == 1 && !(g.c_sn & 1) && !((uintptr_t)g.c & 15) && !(g.M & 1)) {
+        const bool odd = fr & 1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double give = odd ? acc[i][j][0] : acc[i][j][1];
+                const double got = __shfl_xor_sync(0xffffffffu, give, 4);
+                const int64_t m = m0 + wm + i * 8 + (fr & ~1), n = n0 + wn + j * 8 + 2 * fc + (odd ? 1 : 0);
+                if (m >= g.M || n >= g.N) continue;
+                const double v0 = odd ? got : acc[i][j][0], v1 = odd ? acc[i][j][1] : got;
+                double2 *pc = reinterpret_cast<double2 *>(g.c + m + n * g.c_sn);
+                double2 c2 = *pc;
+                c2.x = __dsub_rn(c2.x, v0);
+                c2.y = __dsub_rn(c2.y, v1);
+                *pc = c2;
+            }
+        return;
+    }
     // epilogue: C fragment (row fr, cols 2*fc, 2*fc+1)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
